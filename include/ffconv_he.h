@@ -1,0 +1,136 @@
+/*
+ * ffconv_he.h -- C ABI of the packed RNS-BFV evaluator (drop-in boundary).
+ *
+ * The reference (cipherpack, pure Python) has no FFI: its operator boundary is
+ * the Python class `HeContext` (/root/reference/pkg/src/cipherpack/hesim.py:186-366),
+ * constructed once per run at runner.py:297.  Every entry point below backs one
+ * of its methods; the Python mirror (paper_2102_03494_b200/hesim.py) binds these
+ * symbols through ctypes and keeps counters, depths and error behaviour in Python.
+ *
+ *   fhe_encode        <- HeContext.encode            hesim.py:203-215
+ *   fhe_encrypt       <- HeContext.encrypt           hesim.py:217-219
+ *   fhe_ct_zero       <- HeContext.encrypt_zero      hesim.py:221-225
+ *   fhe_decrypt       <- HeContext.decrypt           hesim.py:231-238
+ *   fhe_rotate(_many) <- HeContext.rotate            hesim.py:244-261
+ *   fhe_mul_plain(_many) <- HeContext.mul_plain      hesim.py:263-302
+ *   fhe_mul_scalar    <- mul_plain by a constant     engine.py:92-97,189-195 (conv_conv)
+ *   fhe_add(_many)    <- HeContext.add_cc            hesim.py:304-316
+ *   fhe_add_plain     <- HeContext.add_plain         hesim.py:318-326
+ *   fhe_square        <- HeContext.square            hesim.py:328-345
+ *   fhe_mod_switch    <- (no reference counterpart; BASELINE cfg1 "rescale")
+ *
+ * Scheme: RNS-BFV over Z[X]/(X^n+1).  One ciphertext "slot row" of the reference
+ * (n_slots = N) is one batching row of a ring of degree n = 2N; row 0 and row 1
+ * carry two independent slot vectors (two images).  Plaintext moduli may be a
+ * list t_0..t_{T-1} (plaintext CRT): a ciphertext object holds T x R physical
+ * ciphertexts laid out [T][R][2][level][n] (uint64, NTT domain, limb-major).
+ *
+ * Conventions (shared bit-for-bit by the CUDA library and the golden C model in
+ * oracle/golden_rlwe.c) are documented in DESIGN.md section "Golden spec".
+ *
+ * All functions return 0 on success and a negative code on failure; the message
+ * is available from fhe_last_error().  No C++ exceptions cross this boundary.
+ */
+#ifndef FFCONV_HE_H
+#define FFCONV_HE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FHE_MAX_Q 24   /* ciphertext primes q_0..q_{L-1}             */
+#define FHE_MAX_P 2    /* special (key-switching) primes              */
+#define FHE_MAX_B 26   /* auxiliary primes for ct x ct multiplication */
+#define FHE_MAX_T 8    /* plaintext CRT moduli                        */
+
+#define FHE_OK 0
+#define FHE_EINVAL -1
+#define FHE_ENOMEM -2
+#define FHE_EDEVICE -3
+#define FHE_ELEVEL -4
+
+typedef struct fhe_params {
+    uint32_t log_n;   /* ring degree n = 2^log_n (3 <= log_n <= 14); N = n/2 slots per row */
+    uint32_t L;       /* ciphertext primes at the top level                              */
+    uint32_t K;       /* special primes (must be 1)                                      */
+    uint32_t n_aux;   /* auxiliary base size for fhe_square (0 disables squaring)         */
+    uint32_t T;       /* plaintext moduli                                                */
+    uint32_t flags;   /* reserved, 0                                                     */
+    uint64_t q[FHE_MAX_Q];
+    uint64_t p[FHE_MAX_P];
+    uint64_t b[FHE_MAX_B];
+    uint64_t t[FHE_MAX_T];
+    uint64_t seed;    /* all key material and encryption randomness derive from it       */
+    int32_t device;   /* CUDA device ordinal (ignored by the golden model)               */
+    int32_t reserved;
+} fhe_params;
+
+typedef struct fhe_ctx fhe_ctx;
+typedef struct fhe_ct fhe_ct;
+typedef struct fhe_pt fhe_pt;
+
+const char *fhe_last_error(void);
+const char *fhe_backend_name(void);   /* "cuda-sm100a" or "golden-c" */
+
+int fhe_ctx_create(const fhe_params *params, fhe_ctx **out);
+void fhe_ctx_destroy(fhe_ctx *ctx);
+int fhe_sync(fhe_ctx *ctx);
+/* bytes of device (or host, golden) memory held by keys and tables */
+int fhe_ctx_key_bytes(fhe_ctx *ctx, uint64_t *out);
+/* generate Galois keys for the given rotation steps now (otherwise lazily) */
+int fhe_keygen_rotations(fhe_ctx *ctx, const uint32_t *steps, uint32_t m);
+
+/* ---- ciphertext objects ------------------------------------------------ */
+/* R row-pairs (two slot vectors each) per plaintext modulus; level in [1, L]. */
+int fhe_ct_create(fhe_ctx *ctx, uint32_t R, uint32_t level, fhe_ct **out);
+void fhe_ct_destroy(fhe_ct *ct);
+uint32_t fhe_ct_level(const fhe_ct *ct);
+uint32_t fhe_ct_rows(const fhe_ct *ct);
+/* raw NTT-domain words, [T*R][2][level][n] */
+int fhe_ct_read(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *words);
+int fhe_ct_write(fhe_ctx *ctx, fhe_ct *ct, const uint64_t *words);
+/* transparent encryption of zero: (0, 0) */
+int fhe_ct_zero(fhe_ctx *ctx, fhe_ct *ct);
+
+/* ---- plaintexts --------------------------------------------------------- */
+int fhe_pt_create(fhe_ctx *ctx, fhe_pt **out);
+void fhe_pt_destroy(fhe_pt *pt);
+/* slots: [T][n] residues mod t_k; position r*N + i is row r, slot i */
+int fhe_encode(fhe_ctx *ctx, const uint64_t *slots, fhe_pt *out);
+/* [T][L][n] NTT-domain words of the lifted plaintext */
+int fhe_pt_read(fhe_ctx *ctx, const fhe_pt *pt, uint64_t *words);
+
+/* ---- client side ---------------------------------------------------------- */
+/* slots: [T][R][n] residues; secret-key encryption at the top level.  Each call
+ * must use a fresh nonce (the randomness is a pure function of seed, nonce and
+ * the physical ciphertext index). */
+int fhe_encrypt(fhe_ctx *ctx, const uint64_t *slots, uint32_t nonce, fhe_ct *out);
+int fhe_decrypt(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *slots);
+/* diagnostic: coefficient-form x = c0 + c1*s over Q_level, [T*R][level][n]
+ * (the caller derives the exact invariant noise |[t x]_Q| / Q from it) */
+int fhe_decrypt_raw(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *coef);
+
+/* ---- evaluation (out may alias an input unless stated) --------------------- */
+int fhe_add(fhe_ctx *ctx, const fhe_ct *a, const fhe_ct *b, fhe_ct *out);
+int fhe_mul_plain(fhe_ctx *ctx, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out);
+int fhe_mul_scalar(fhe_ctx *ctx, const fhe_ct *a, int64_t w, fhe_ct *out);
+int fhe_add_plain(fhe_ctx *ctx, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out);
+/* left rotation of both rows by k in [1, N): Galois element 5^k mod 2n, then
+ * hybrid key switching; out must not alias a */
+int fhe_rotate(fhe_ctx *ctx, const fhe_ct *a, uint32_t k, fhe_ct *out);
+/* drop the last prime with rounding; out must have level = a.level - 1 */
+int fhe_mod_switch(fhe_ctx *ctx, const fhe_ct *a, fhe_ct *out);
+/* slot-wise square with relinearization; out must not alias a */
+int fhe_square(fhe_ctx *ctx, const fhe_ct *a, fhe_ct *out);
+
+/* batched forms: m independent operations in one launch sequence */
+int fhe_rotate_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k);
+int fhe_mul_plain_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m);
+int fhe_add_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *b, fhe_ct *const *out, uint32_t m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFCONV_HE_H */

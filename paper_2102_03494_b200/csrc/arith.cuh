@@ -1,0 +1,152 @@
+// arith.cuh -- modular arithmetic, fixed-point sums and ChaCha20 samplers for
+// the sm_100a evaluator.  Integer pipes only: 64-bit words, primes < 2^61.
+//
+//  * Shoup multiplication (fixed operand w with w' = floor(w 2^64 / q)) for NTT
+//    twiddles and per-prime scalars: mul.lo + mul.hi + mul.lo, lazy in [0, 2q).
+//  * Montgomery multiplication (R = 2^64) for operand pairs that are both
+//    data (ct x pt, key inner products): operands stored pre-scaled by R.
+//  * 64-bit Barrett-style reduction with mu = floor(2^64 / q).
+//
+// The sampler conventions (block layout, domains, CBD(21), ternary mod 3) are
+// the golden spec shared with oracle/golden_rlwe.c.
+#pragma once
+#include <cstdint>
+
+typedef uint64_t u64;
+typedef uint32_t u32;
+typedef int64_t i64;
+typedef unsigned __int128 u128;
+
+#define DEV __device__ __forceinline__
+#define HD __host__ __device__ __forceinline__
+
+struct ModInfo {
+    u64 q;
+    u64 qinv;      // q^-1 mod 2^64 (Montgomery)
+    u64 r2;        // 2^128 mod q
+    u64 mu;        // floor(2^64 / q)
+    u64 ninv, ninv_sh;
+    u64 half;      // (q - 1) / 2
+    const u64 *tw, *tw_sh;     // psi^brev(k)  and Shoup companions
+    const u64 *itw, *itw_sh;   // psi^-brev(k) and Shoup companions
+};
+
+DEV u64 mulhi(u64 a, u64 b) { return __umul64hi(a, b); }
+
+// a*w mod q in [0, 2q), any 64-bit a
+DEV u64 shoup_lazy(u64 a, u64 w, u64 wsh, u64 q) { return a * w - mulhi(a, wsh) * q; }
+DEV u64 shoup(u64 a, u64 w, u64 wsh, u64 q) {
+    u64 r = shoup_lazy(a, w, wsh, q);
+    return r >= q ? r - q : r;
+}
+// a*b*2^-64 mod q, canonical; requires a*b < q*2^64 (e.g. b < q)
+DEV u64 mont(u64 a, u64 b, u64 q, u64 qinv) {
+    u64 lo = a * b, hi = mulhi(a, b);
+    u64 m = lo * qinv;
+    u64 mh = mulhi(m, q);
+    return hi >= mh ? hi - mh : hi - mh + q;
+}
+DEV u64 addm(u64 a, u64 b, u64 q) { u64 s = a + b; return s >= q ? s - q : s; }
+DEV u64 subm(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+DEV u64 negm(u64 a, u64 q) { return a ? q - a : 0; }
+// x mod q for any 64-bit x
+DEV u64 red64(u64 x, u64 q, u64 mu) {
+    u64 r = x - mulhi(x, mu) * q;
+    while (r >= q) r -= q;
+    return r;
+}
+// a*b mod q for a, b < q (two Montgomery steps)
+DEV u64 mulmod(u64 a, u64 b, const ModInfo &M) { return mont(mont(a, b, M.q, M.qinv), M.r2, M.q, M.qinv); }
+DEV u64 to_mont(u64 a, const ModInfo &M) { return mont(a, M.r2, M.q, M.qinv); }
+// signed -> [0, q)
+DEV u64 smod(i64 v, const ModInfo &M) {
+    if (v >= 0) return red64((u64)v, M.q, M.mu);
+    u64 r = red64((u64)(-(v + 1)), M.q, M.mu);
+    return M.q - 1 - r;
+}
+// x in [0, m_src) read as centered (x > (m_src-1)/2 -> x - m_src), then mod q;
+// msrc_q = m_src mod q
+DEV u64 centered_lift(u64 x, u64 half_src, u64 msrc_q, const ModInfo &M) {
+    u64 r = red64(x, M.q, M.mu);
+    return x > half_src ? subm(r, msrc_q, M.q) : r;
+}
+// x (128-bit) mod q
+DEV u64 mod128(u128 x, const ModInfo &M) {
+    u64 hi = red64((u64)(x >> 64), M.q, M.mu), lo = red64((u64)x, M.q, M.mu);
+    // 2^64 mod q = mont(r2, 1) ... use r2 = 2^128 mod q: hi * 2^64 = mont(hi, r2)
+    return addm(mont(hi, M.r2, M.q, M.qinv), lo, M.q);
+}
+
+// accumulate y * (W + F / 2^128) into (ai, af) exactly (golden: fx_acc)
+DEV void fx_acc(u128 &ai, u128 &af, u64 y, u64 W, u64 Fhi, u64 Flo) {
+    u128 p_lo = (u128)y * Flo;
+    u128 p_hi = (u128)y * Fhi;
+    u128 low = p_lo + (p_hi << 64);
+    u128 c1 = low < p_lo;
+    u128 ip = (p_hi >> 64) + c1;
+    af += low;
+    u128 c2 = af < low;
+    ai += (u128)y * W + ip + c2;
+}
+
+// ------------------------------------------------------------------ ChaCha20
+enum { DOM_SK = 1, DOM_ENC_A = 2, DOM_ENC_E = 3, DOM_KSK_A = 4, DOM_KSK_E = 5 };
+
+DEV u32 rotl32(u32 a, int b) { return __funnelshift_l(a, a, b); }
+#define CQR(a, b, c, d)                      \
+    a += b; d ^= a; d = rotl32(d, 16);       \
+    c += d; b ^= c; b = rotl32(b, 12);       \
+    a += b; d ^= a; d = rotl32(d, 8);        \
+    c += d; b ^= c; b = rotl32(b, 7);
+
+DEV void chacha_block(u32 out[16], u64 seed, u32 ctr, u32 dom, u32 sub, u32 x, u32 y) {
+    u32 in[16] = {0x61707865u, 0x3320646eu, 0x79622d32u, 0x6b206574u,
+                  (u32)seed, (u32)(seed >> 32), 0x243F6A88u, 0x85A308D3u,
+                  0x13198A2Eu, 0x03707344u, 0xA4093822u, 0x299F31D0u,
+                  ctr, (dom << 24) | (sub & 0xFFFFFFu), x, y};
+    u32 s[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) s[i] = in[i];
+#pragma unroll 1
+    for (int i = 0; i < 10; i++) {
+        CQR(s[0], s[4], s[8], s[12]);
+        CQR(s[1], s[5], s[9], s[13]);
+        CQR(s[2], s[6], s[10], s[14]);
+        CQR(s[3], s[7], s[11], s[15]);
+        CQR(s[0], s[5], s[10], s[15]);
+        CQR(s[1], s[6], s[11], s[12]);
+        CQR(s[2], s[7], s[8], s[13]);
+        CQR(s[3], s[4], s[9], s[14]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; i++) out[i] = s[i] + in[i];
+}
+
+// uniform residue for coefficient c (words 4(c%4)..+3 of block c/4)
+DEV u64 sample_uniform(const ModInfo &M, u64 seed, u32 dom, u32 sub, u32 x, u32 y, u32 c) {
+    u32 blk[16];
+    chacha_block(blk, seed, c >> 2, dom, sub, x, y);
+    const int o = 4 * (c & 3);
+    u128 v = ((u128)blk[o + 3] << 96) | ((u128)blk[o + 2] << 64) | ((u128)blk[o + 1] << 32) | blk[o];
+    return mod128(v, M);
+}
+DEV int sample_ternary(u64 seed, u32 dom, u32 sub, u32 x, u32 y, u32 c) {
+    u32 blk[16];
+    chacha_block(blk, seed, c >> 4, dom, sub, x, y);
+    u32 r = blk[c & 15] % 3u;
+    return r == 2 ? -1 : (int)r;
+}
+DEV int sample_cbd(u64 seed, u32 dom, u32 sub, u32 x, u32 y, u32 c) {
+    u32 blk[16];
+    chacha_block(blk, seed, c >> 3, dom, sub, x, y);
+    u32 w0 = blk[2 * (c & 7)] & 0x1FFFFFu, w1 = blk[2 * (c & 7) + 1] & 0x1FFFFFu;
+    return __popc(w0) - __popc(w1);
+}
+
+DEV u32 brev_n(u32 x, int logn) { return __brev(x) >> (32 - logn); }
+// NTT-domain automorphism X -> X^g: out[j] = in[perm(j)]
+DEV u32 galois_perm(u32 j, u32 g, int logn) {
+    u32 e = 2u * brev_n(j, logn) + 1u;
+    u32 eg = (u32)(((u64)e * g) & ((2ull << logn) - 1));
+    return brev_n((eg - 1u) >> 1, logn);
+}

@@ -1,0 +1,1004 @@
+// ffconv_he.cu -- host side of the sm_100a packed RNS-BFV evaluator: context,
+// tables, memory, and the C ABI of include/ffconv_he.h.
+//
+// One context = one CUDA stream; every entry point enqueues asynchronously except
+// read/decrypt/sync, which block.  Ciphertexts live in stream-ordered pool
+// allocations, limb-major [T*R][2][level][n] uint64 in the NTT domain.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "ffconv_he.h"
+#include "kernels.cuh"
+
+// =================================================================== errors
+static thread_local char g_err[512];
+static int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+#define CU(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(FHE_EDEVICE, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                 \
+    } while (0)
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+#define TRY(x)                  \
+    do {                        \
+        int rc_ = (x);          \
+        if (rc_) return rc_;    \
+    } while (0)
+
+extern "C" const char *fhe_last_error(void) { return g_err; }
+extern "C" const char *fhe_backend_name(void) { return "cuda-sm100a"; }
+
+// ============================================================ host arithmetic
+namespace hm {
+static u64 mul(u64 a, u64 b, u64 m) { return (u64)((u128)a * b % m); }
+static u64 pw(u64 a, u64 e, u64 m) {
+    u64 r = 1 % m;
+    a %= m;
+    while (e) {
+        if (e & 1) r = mul(r, a, m);
+        a = mul(a, a, m);
+        e >>= 1;
+    }
+    return r;
+}
+static u64 inv(u64 a, u64 m) { return pw(a % m, m - 2, m); }
+static u64 neg(u64 a, u64 m) { return a % m ? m - a % m : 0; }
+static u64 shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+static u64 mont(u64 x, u64 q) { return (u64)(((u128)(x % q) << 64) % q); }
+static void frac128(u64 r, u64 m, u64 &hi, u64 &lo) {   // floor(r 2^128 / m), r < m
+    u128 num = (u128)r << 64;
+    hi = (u64)(num / m);
+    u64 rem = (u64)(num % m);
+    lo = (u64)(((u128)rem << 64) / m);
+}
+static int is_prime(u64 n) {
+    static const u64 bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    if (n < 2) return 0;
+    for (u64 b : bases) {
+        if (n == b) return 1;
+        if (n % b == 0) return 0;
+    }
+    u64 d = n - 1;
+    int s = 0;
+    while (!(d & 1)) { d >>= 1; s++; }
+    for (u64 b : bases) {
+        u64 x = pw(b, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int r = 1; r < s; r++) {
+            x = mul(x, x, n);
+            if (x == n - 1) { comp = false; break; }
+        }
+        if (comp) return 0;
+    }
+    return 1;
+}
+static u32 brev(u32 x, u32 bits) {
+    u32 r = 0;
+    for (u32 i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+static u64 min_root(u64 q, u32 n) {      // minimal primitive 2n-th root of unity
+    u64 two_n = 2ull * n, psi0 = 0;
+    for (u64 h = 2; h < q; h++) {
+        u64 c = pw(h, (q - 1) / two_n, q);
+        if (pw(c, n, q) == q - 1) { psi0 = c; break; }
+    }
+    u64 sq = mul(psi0, psi0, q), cur = psi0, best = psi0;
+    for (u32 k = 0; k < n; k++) {
+        if (cur < best) best = cur;
+        cur = mul(cur, sq, q);
+    }
+    return best;
+}
+}  // namespace hm
+
+// ================================================================== context
+struct KeyBuf {
+    u64 *d = nullptr;   // [L][2][L+1][n], Montgomery form
+};
+
+struct fhe_ctx {
+    fhe_params P{};
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    u32 n = 0, logn = 0, N = 0, L = 0, nb = 0, T = 0, nmod = 0;
+    int special_id = 0, b_id0 = 0, t_id0 = 0;
+    std::vector<u64> mods;             // modulus value per id
+    std::vector<ModInfo> hmods;        // with device twiddle pointers
+    ModInfo *d_mods = nullptr;
+    u64 *d_tw = nullptr;
+    u64 *d_s_can = nullptr, *d_s_m = nullptr, *d_s2_m = nullptr;   // [L+1+nb][n], s2 rows [L+1]
+    unsigned char *d_sk_ids = nullptr;
+    u32 *d_slot2ntt = nullptr, *d_ntt2slot = nullptr;
+    std::vector<LevelDev> hlv;         // index by level 1..L
+    LevelDev *d_lv = nullptr;
+    AuxDev hax{};
+    AuxDev *d_ax = nullptr;
+    u64 *d_pmod = nullptr;             // P mod prime_i, i in [0, L]
+    u64 pinv[MAXQ]{}, pinv_sh[MAXQ]{};
+    std::unordered_map<u32, KeyBuf> keys;
+    u64 key_bytes = 0;
+    // workspaces
+    int S = 1;                          // key-switching sub-batch
+    u64 *w_D = nullptr, *w_C0 = nullptr, *w_C1 = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;
+    u64 *w_sq = nullptr;
+    size_t w_sq_words = 0;
+    u64 *w_tmp = nullptr;
+    size_t w_tmp_words = 0;
+};
+
+struct fhe_ct {
+    fhe_ctx *ctx;
+    u32 R, level, count;
+    u64 *d;
+};
+
+struct fhe_pt {
+    fhe_ctx *ctx;
+    u64 *coef_t;   // [T][n]
+    u64 *ntt_m;    // [T][L][n] Montgomery form
+    int encoded;
+};
+
+static size_t ct_words(const fhe_ct *ct) { return (size_t)ct->count * 2 * ct->level * ct->ctx->n; }
+
+static inline long long nblocks(long long total, int bs = 256) {
+    long long b = (total + bs - 1) / bs;
+    return b > 148 * 16 ? 148 * 16 : (b < 1 ? 1 : b);
+}
+#define EW(kernel, total, ...) kernel<<<(unsigned)nblocks(total), 256, 0, c->st>>>(__VA_ARGS__)
+
+// ----------------------------------------------------- row-kernel dispatch
+static std::mutex g_attr_mu;
+static std::unordered_set<const void *> g_attr_done;
+
+template <int LOGN, typename... KArgs, typename... Args>
+static void launch_row(void (*kern)(KArgs...), dim3 grid, cudaStream_t st, Args... args) {
+    using C = NttCfg<LOGN>;
+    const size_t smem = (size_t)C::SMEM_WORDS * sizeof(u64);
+    {
+        std::lock_guard<std::mutex> lk(g_attr_mu);
+        if (!g_attr_done.count((const void *)kern)) {
+            cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            g_attr_done.insert((const void *)kern);
+        }
+    }
+    kern<<<grid, C::TH, smem, st>>>(args...);
+}
+
+#define LOGN_SWITCH(logn, BODY)                \
+    switch (logn) {                            \
+        case 2: { constexpr int LG = 2; BODY; } break;   \
+        case 3: { constexpr int LG = 3; BODY; } break;   \
+        case 4: { constexpr int LG = 4; BODY; } break;   \
+        case 5: { constexpr int LG = 5; BODY; } break;   \
+        case 6: { constexpr int LG = 6; BODY; } break;   \
+        case 7: { constexpr int LG = 7; BODY; } break;   \
+        case 8: { constexpr int LG = 8; BODY; } break;   \
+        case 9: { constexpr int LG = 9; BODY; } break;   \
+        case 10: { constexpr int LG = 10; BODY; } break; \
+        case 11: { constexpr int LG = 11; BODY; } break; \
+        case 12: { constexpr int LG = 12; BODY; } break; \
+        case 13: { constexpr int LG = 13; BODY; } break; \
+        case 14: { constexpr int LG = 14; BODY; } break; \
+        default: break;                        \
+    }
+
+static int ntt_rows(fhe_ctx *c, int rows, const NttRowsArgs &a) {
+    if (rows <= 0) return 0;
+    LOGN_SWITCH(c->logn, launch_row<LG>(k_ntt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
+    CHECK_LAUNCH();
+    return 0;
+}
+static int intt_rows(fhe_ctx *c, int rows, const InttRowsArgs &a) {
+    if (rows <= 0) return 0;
+    LOGN_SWITCH(c->logn, launch_row<LG>(k_intt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
+    CHECK_LAUNCH();
+    return 0;
+}
+
+static NttRowsArgs nargs(const u64 *src, u64 *dst, long long stride) {
+    NttRowsArgs a;
+    memset(&a, 0, sizeof a);
+    a.src = src; a.dst = dst; a.rdiv = 1; a.sA = stride; a.dA = stride;
+    a.div = 1; a.period = 1; a.div2 = 1; a.period2 = 1;
+    return a;
+}
+static InttRowsArgs iargs(const u64 *src, u64 *dst, long long stride) {
+    InttRowsArgs a;
+    memset(&a, 0, sizeof a);
+    a.src = src; a.dst = dst; a.rdiv = 1; a.sA = stride; a.dA = stride;
+    a.div = 1; a.period = 1;
+    return a;
+}
+static void map_range(ModMap &m, u32 period, int base) { for (u32 i = 0; i < period; i++) m.id[i] = (unsigned char)(base + i); }
+static void map_q(ModMap &m, u32 l) { map_range(m, l, 0); }
+
+static int ensure_tmp(fhe_ctx *c, size_t words) {
+    if (words <= c->w_tmp_words) return 0;
+    if (c->w_tmp) CU(cudaFreeAsync(c->w_tmp, c->st));
+    CU(cudaMallocAsync((void **)&c->w_tmp, words * 8, c->st));
+    c->w_tmp_words = words;
+    return 0;
+}
+
+// ------------------------------------------------------------- validation
+static int validate(const fhe_params *p) {
+    if (p->log_n < 2 || p->log_n > 14) return fail(FHE_EINVAL, "log_n must be in [2, 14] (got %u)", p->log_n);
+    if (p->L < 1 || p->L > FHE_MAX_Q) return fail(FHE_EINVAL, "L must be in [1, %d]", FHE_MAX_Q);
+    if (p->K != 1) return fail(FHE_EINVAL, "exactly one special prime is supported (K=%u)", p->K);
+    if (p->n_aux > FHE_MAX_B) return fail(FHE_EINVAL, "n_aux must be <= %d", FHE_MAX_B);
+    if (p->n_aux && p->n_aux < p->L + 1) return fail(FHE_EINVAL, "n_aux must be 0 or >= L+1");
+    if (p->T < 1 || p->T > FHE_MAX_T) return fail(FHE_EINVAL, "T must be in [1, %d]", FHE_MAX_T);
+    u64 two_n = 2ull << p->log_n;
+    std::vector<u64> all;
+    for (u32 i = 0; i < p->L; i++) all.push_back(p->q[i]);
+    all.push_back(p->p[0]);
+    for (u32 i = 0; i < p->n_aux; i++) all.push_back(p->b[i]);
+    for (u32 i = 0; i < p->T; i++) all.push_back(p->t[i]);
+    for (size_t i = 0; i < all.size(); i++) {
+        if (all[i] >= (1ull << 61) || all[i] < 3) return fail(FHE_EINVAL, "modulus %llu outside [3, 2^61)", (unsigned long long)all[i]);
+        if (!hm::is_prime(all[i])) return fail(FHE_EINVAL, "modulus %llu is not prime", (unsigned long long)all[i]);
+        if (all[i] % two_n != 1) return fail(FHE_EINVAL, "modulus %llu is not 1 mod 2n = %llu", (unsigned long long)all[i], (unsigned long long)two_n);
+        for (size_t j = 0; j < i; j++)
+            if (all[j] == all[i]) return fail(FHE_EINVAL, "modulus %llu repeated", (unsigned long long)all[i]);
+    }
+    for (u32 i = 0; i < p->L; i++)
+        if (p->p[0] < p->q[i]) return fail(FHE_EINVAL, "special prime must exceed every q_i");
+    return 0;
+}
+
+// ------------------------------------------------------------- tables
+static void build_level(fhe_ctx *c, u32 l, LevelDev &T) {
+    memset(&T, 0, sizeof T);
+    const u64 *q = c->P.q;
+    for (u32 i = 0; i < l; i++) {
+        u64 qh = 1;
+        for (u32 j = 0; j < l; j++) if (j != i) qh = hm::mul(qh, q[j] % q[i], q[i]);
+        T.Qtilde_m[i] = hm::mont(hm::inv(qh, q[i]), q[i]);
+        hm::frac128(1, q[i], T.invq_hi[i], T.invq_lo[i]);
+        if (l >= 2 && i < l - 1) {
+            T.msinv[i] = hm::inv(q[l - 1] % q[i], q[i]);
+            T.msinv_sh[i] = hm::shoup(T.msinv[i], q[i]);
+            T.qlast_mod[i] = q[l - 1] % q[i];
+        }
+    }
+    T.half_last = (q[l - 1] - 1) / 2;
+    for (u32 k = 0; k < c->T; k++) {
+        u64 t = c->P.t[k], rt = 1;
+        for (u32 j = 0; j < l; j++) rt = hm::mul(rt, q[j] % t, t);
+        T.rt[k] = rt;
+        T.rtF[k] = (u64)(((u128)rt << 64) / t);
+        for (u32 i = 0; i < l; i++) {
+            T.decW[k][i] = t / q[i];
+            hm::frac128(t % q[i], q[i], T.decFhi[k][i], T.decFlo[k][i]);
+            u64 delta = hm::mul(hm::neg(rt, q[i]), hm::inv(t % q[i], q[i]), q[i]);
+            T.delta_m[k][i] = hm::mont(delta, q[i]);
+        }
+    }
+    if (!c->nb) return;
+    const u64 *b = c->P.b;
+    u32 nb = c->nb;
+    for (u32 k = 0; k < nb; k++) {
+        u64 Qm = 1;
+        for (u32 j = 0; j < l; j++) Qm = hm::mul(Qm, q[j] % b[k], b[k]);
+        T.QmodB_m[k] = hm::mont(Qm, b[k]);
+        for (u32 i = 0; i < l; i++) {
+            u64 qh = 1;
+            for (u32 j = 0; j < l; j++) if (j != i) qh = hm::mul(qh, q[j] % b[k], b[k]);
+            T.QhatB_m[i][k] = hm::mont(qh, b[k]);
+        }
+        u64 bh = 1;
+        for (u32 j = 0; j < nb; j++) if (j != k) bh = hm::mul(bh, b[j] % b[k], b[k]);
+        T.Mtb_m[k] = hm::mont(hm::inv(hm::mul(bh, Qm, b[k]), b[k]), b[k]);
+    }
+    for (u32 i = 0; i < l; i++) {
+        u64 Bm = 1;
+        for (u32 k = 0; k < nb; k++) Bm = hm::mul(Bm, b[k] % q[i], q[i]);
+        u64 qh = 1;
+        for (u32 j = 0; j < l; j++) if (j != i) qh = hm::mul(qh, q[j] % q[i], q[i]);
+        T.Mtq_m[i] = hm::mont(hm::inv(hm::mul(qh, Bm, q[i]), q[i]), q[i]);
+        for (u32 kt = 0; kt < c->T; kt++) {
+            u64 t = c->P.t[kt];
+            u64 tBq = hm::mul(t % q[i], Bm, q[i]);
+            hm::frac128(tBq, q[i], T.theta_hi[kt][i], T.theta_lo[kt][i]);
+            for (u32 k = 0; k < nb; k++) {
+                u64 om = hm::mul(hm::neg(tBq % b[k], b[k]), hm::inv(q[i] % b[k], b[k]), b[k]);
+                T.omega_m[kt][i][k] = hm::mont(om, b[k]);
+            }
+        }
+    }
+    for (u32 kt = 0; kt < c->T; kt++) {
+        u64 t = c->P.t[kt];
+        for (u32 k = 0; k < nb; k++) {
+            u64 bh = 1;
+            for (u32 j = 0; j < nb; j++) if (j != k) bh = hm::mul(bh, b[j] % b[k], b[k]);
+            T.tBb_m[kt][k] = hm::mont(hm::mul(t % b[k], bh, b[k]), b[k]);
+        }
+    }
+}
+
+static void build_aux(fhe_ctx *c, AuxDev &A) {
+    memset(&A, 0, sizeof A);
+    const u64 *b = c->P.b, *q = c->P.q;
+    for (u32 k = 0; k < c->nb; k++) {
+        u64 bh = 1;
+        for (u32 j = 0; j < c->nb; j++) if (j != k) bh = hm::mul(bh, b[j] % b[k], b[k]);
+        A.Btilde_m[k] = hm::mont(hm::inv(bh, b[k]), b[k]);
+        hm::frac128(1, b[k], A.invb_hi[k], A.invb_lo[k]);
+        for (u32 i = 0; i < c->L; i++) {
+            u64 h = 1;
+            for (u32 j = 0; j < c->nb; j++) if (j != k) h = hm::mul(h, b[j] % q[i], q[i]);
+            A.BhatQ_m[k][i] = hm::mont(h, q[i]);
+        }
+    }
+    for (u32 i = 0; i < c->L; i++) {
+        u64 Bm = 1;
+        for (u32 k = 0; k < c->nb; k++) Bm = hm::mul(Bm, b[k] % q[i], q[i]);
+        A.BmodQ_m[i] = hm::mont(Bm, q[i]);
+    }
+}
+
+static int setup_moduli(fhe_ctx *c) {
+    u32 n = c->n;
+    c->nmod = c->L + 1 + c->nb + c->T;
+    c->special_id = c->L;
+    c->b_id0 = c->L + 1;
+    c->t_id0 = c->L + 1 + c->nb;
+    c->mods.clear();
+    for (u32 i = 0; i < c->L; i++) c->mods.push_back(c->P.q[i]);
+    c->mods.push_back(c->P.p[0]);
+    for (u32 i = 0; i < c->nb; i++) c->mods.push_back(c->P.b[i]);
+    for (u32 i = 0; i < c->T; i++) c->mods.push_back(c->P.t[i]);
+    std::vector<u64> tw((size_t)c->nmod * 4 * n);
+    CU(cudaMalloc((void **)&c->d_tw, tw.size() * 8));
+    c->hmods.resize(c->nmod);
+    std::vector<u64> pw(n), pwi(n);
+    for (u32 id = 0; id < c->nmod; id++) {
+        u64 q = c->mods[id];
+        u64 psi = hm::min_root(q, n), psi_inv = hm::inv(psi, q);
+        pw[0] = 1; pwi[0] = 1;
+        for (u32 k = 1; k < n; k++) { pw[k] = hm::mul(pw[k - 1], psi, q); pwi[k] = hm::mul(pwi[k - 1], psi_inv, q); }
+        u64 *base = tw.data() + (size_t)id * 4 * n;
+        for (u32 k = 0; k < n; k++) {
+            u64 w = pw[hm::brev(k, c->logn)], wi = pwi[hm::brev(k, c->logn)];
+            base[k] = w;
+            base[n + k] = hm::shoup(w, q);
+            base[2 * n + k] = wi;
+            base[3 * n + k] = hm::shoup(wi, q);
+        }
+        ModInfo &M = c->hmods[id];
+        M.q = q;
+        u64 x = q;                         // Newton: q^-1 mod 2^64
+        for (int it = 0; it < 6; it++) x *= 2 - q * x;
+        M.qinv = x;
+        u64 r1 = (u64)(((u128)1 << 64) % q);
+        M.r2 = hm::mul(r1, r1, q);
+        M.mu = (u64)(((u128)1 << 64) / q);
+        M.ninv = hm::inv(n, q);
+        M.ninv_sh = hm::shoup(M.ninv, q);
+        M.half = (q - 1) / 2;
+        u64 *dbase = c->d_tw + (size_t)id * 4 * n;
+        M.tw = dbase; M.tw_sh = dbase + n; M.itw = dbase + 2 * n; M.itw_sh = dbase + 3 * n;
+    }
+    CU(cudaMemcpy(c->d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
+    CU(cudaMalloc((void **)&c->d_mods, c->nmod * sizeof(ModInfo)));
+    CU(cudaMemcpy(c->d_mods, c->hmods.data(), c->nmod * sizeof(ModInfo), cudaMemcpyHostToDevice));
+    return 0;
+}
+
+static int setup_secret(fhe_ctx *c) {
+    u32 n = c->n, nks = c->L + 1 + c->nb;
+    std::vector<unsigned char> ids(nks);
+    for (u32 r = 0; r < nks; r++) ids[r] = (unsigned char)r;   // q..., special, aux... (ids coincide)
+    CU(cudaMalloc((void **)&c->d_sk_ids, nks));
+    CU(cudaMemcpy(c->d_sk_ids, ids.data(), nks, cudaMemcpyHostToDevice));
+    CU(cudaMalloc((void **)&c->d_s_can, (size_t)nks * n * 8));
+    CU(cudaMalloc((void **)&c->d_s_m, (size_t)nks * n * 8));
+    CU(cudaMalloc((void **)&c->d_s2_m, (size_t)(c->L + 1) * n * 8));
+    long long total = (long long)nks * n;
+    EW(k_sk_prep, total, c->d_s_can, total, (int)c->logn, c->P.seed, c->d_sk_ids, c->d_mods);
+    CHECK_LAUNCH();
+    NttRowsArgs a = nargs(c->d_s_can, c->d_s_can, n);
+    a.period = nks;
+    map_range(a.map, nks, 0);
+    TRY(ntt_rows(c, nks, a));
+    EW(k_sk_finish, total, c->d_s_can, c->d_s_m, c->d_s2_m, total, (int)(c->L + 1), (int)c->logn, c->d_sk_ids,
+       c->d_mods);
+    CHECK_LAUNCH();
+    // P mod prime_i and P^-1 mod q_i
+    std::vector<u64> pm(c->L + 1);
+    u64 P = c->P.p[0];
+    for (u32 i = 0; i <= c->L; i++) pm[i] = P % c->mods[i];
+    for (u32 i = 0; i < c->L; i++) {
+        c->pinv[i] = hm::inv(pm[i], c->P.q[i]);
+        c->pinv_sh[i] = hm::shoup(c->pinv[i], c->P.q[i]);
+    }
+    CU(cudaMalloc((void **)&c->d_pmod, (c->L + 1) * 8));
+    CU(cudaMemcpy(c->d_pmod, pm.data(), (c->L + 1) * 8, cudaMemcpyHostToDevice));
+    return 0;
+}
+
+static int setup_workspace(fhe_ctx *c) {
+    size_t n = c->n, L = c->L;
+    size_t per_ct = n * (3 * L + L * (L + 1) + 2 * (L + 1)) * 8;
+    size_t budget = 96ull << 20;   // keep one sub-batch's intermediates L2-sized
+    const char *env = getenv("FHE_KS_BATCH");
+    int S = env ? atoi(env) : (int)(budget / per_ct);
+    if (S < 1) S = 1;
+    if (S > MAXS) S = MAXS;
+    c->S = S;
+    CU(cudaMalloc((void **)&c->w_D, S * L * n * 8));
+    CU(cudaMalloc((void **)&c->w_C0, S * L * n * 8));
+    CU(cudaMalloc((void **)&c->w_C1, S * L * n * 8));
+    CU(cudaMalloc((void **)&c->w_Ext, S * L * (L + 1) * n * 8));
+    CU(cudaMalloc((void **)&c->w_Acc, S * 2 * (L + 1) * n * 8));
+    if (c->nb) {
+        size_t l = L, nb = c->nb;
+        c->w_sq_words = S * n * (2 * l + 2 * nb + 3 * (l + nb) + 3 * l + 3 * l);
+        CU(cudaMalloc((void **)&c->w_sq, c->w_sq_words * 8));
+    }
+    return 0;
+}
+
+extern "C" int fhe_ctx_create(const fhe_params *params, fhe_ctx **out) {
+    TRY(validate(params));
+    fhe_ctx *c = new fhe_ctx();
+    c->P = *params;
+    c->dev = params->device;
+    c->logn = params->log_n;
+    c->n = 1u << c->logn;
+    c->N = c->n / 2;
+    c->L = params->L;
+    c->nb = params->n_aux;
+    c->T = params->T;
+    int rc = 0;
+    do {
+        if (cudaSetDevice(c->dev) != cudaSuccess) { rc = fail(FHE_EDEVICE, "cannot select CUDA device %d", c->dev); break; }
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, c->dev) != cudaSuccess) { rc = fail(FHE_EDEVICE, "no CUDA device"); break; }
+        if (prop.major != 10) { rc = fail(FHE_EDEVICE, "device %s is sm_%d%d; this build targets sm_100a", prop.name, prop.major, prop.minor); break; }
+        if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(FHE_EDEVICE, "stream creation failed"); break; }
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, c->dev) == cudaSuccess) {
+            u64 thresh = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh);
+        }
+        if ((rc = setup_moduli(c))) break;
+        // slot maps
+        std::vector<u32> s2n(c->n), n2s(c->n);
+        u64 two_n = 2ull * c->n, e = 1;
+        for (u32 i = 0; i < c->N; i++) {
+            s2n[i] = hm::brev((u32)((e - 1) / 2), c->logn);
+            s2n[c->N + i] = hm::brev((u32)((two_n - e - 1) / 2), c->logn);
+            e = e * 5 % two_n;
+        }
+        for (u32 x = 0; x < c->n; x++) n2s[s2n[x]] = x;
+        if (cudaMalloc((void **)&c->d_slot2ntt, c->n * 4) || cudaMalloc((void **)&c->d_ntt2slot, c->n * 4)) { rc = fail(FHE_ENOMEM, "cudaMalloc"); break; }
+        cudaMemcpy(c->d_slot2ntt, s2n.data(), c->n * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(c->d_ntt2slot, n2s.data(), c->n * 4, cudaMemcpyHostToDevice);
+        c->hlv.resize(c->L + 1);
+        for (u32 l = 1; l <= c->L; l++) build_level(c, l, c->hlv[l]);
+        if (cudaMalloc((void **)&c->d_lv, (c->L + 1) * sizeof(LevelDev)) != cudaSuccess) { rc = fail(FHE_ENOMEM, "cudaMalloc"); break; }
+        cudaMemcpy(c->d_lv, c->hlv.data(), (c->L + 1) * sizeof(LevelDev), cudaMemcpyHostToDevice);
+        if (c->nb) {
+            build_aux(c, c->hax);
+            cudaMalloc((void **)&c->d_ax, sizeof(AuxDev));
+            cudaMemcpy(c->d_ax, &c->hax, sizeof(AuxDev), cudaMemcpyHostToDevice);
+        }
+        if ((rc = setup_secret(c))) break;
+        if ((rc = setup_workspace(c))) break;
+        if (cudaStreamSynchronize(c->st) != cudaSuccess) { rc = fail(FHE_EDEVICE, "context setup failed: %s", cudaGetErrorString(cudaGetLastError())); break; }
+    } while (0);
+    if (rc) {
+        fhe_ctx_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return 0;
+}
+
+extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    if (c->st) cudaStreamSynchronize(c->st);
+    for (auto &kv : c->keys) cudaFree(kv.second.d);
+    void *bufs[] = {c->d_mods, c->d_tw, c->d_s_can, c->d_s_m, c->d_s2_m, c->d_sk_ids, c->d_slot2ntt,
+                    c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_D, c->w_C0, c->w_C1, c->w_Ext, c->w_Acc, c->w_sq};
+    for (void *b : bufs) if (b) cudaFree(b);
+    if (c->w_tmp) cudaFreeAsync(c->w_tmp, c->st);
+    if (c->st) { cudaStreamSynchronize(c->st); cudaStreamDestroy(c->st); }
+    delete c;
+}
+
+extern "C" int fhe_sync(fhe_ctx *c) {
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+extern "C" int fhe_ctx_key_bytes(fhe_ctx *c, uint64_t *out) {
+    *out = c->key_bytes;
+    return 0;
+}
+
+// ===================================================================== keys
+static u32 galois_elt(const fhe_ctx *c, u32 k) { return (u32)hm::pw(5, k, 2ull * c->n); }
+
+static int get_key(fhe_ctx *c, u32 kid, const u64 **out) {
+    auto it = c->keys.find(kid);
+    if (it != c->keys.end()) { *out = it->second.d; return 0; }
+    size_t n = c->n, L = c->L;
+    size_t words = L * 2 * (L + 1) * n;
+    KeyBuf kb;
+    CU(cudaMalloc((void **)&kb.d, words * 8));
+    TRY(ensure_tmp(c, L * (L + 1) * n));
+    long long total = (long long)L * (L + 1) * n;
+    EW(k_key_prep, total, c->w_tmp, total, (int)L, (int)c->logn, c->P.seed, kid, c->special_id, c->d_mods);
+    CHECK_LAUNCH();
+    NttRowsArgs a = nargs(c->w_tmp, c->w_tmp, n);
+    a.period = L + 1;
+    map_range(a.map, L + 1, 0);   // ids 0..L-1 = q, L = special
+    TRY(ntt_rows(c, (int)(L * (L + 1)), a));
+    EW(k_key_finish, total, c->w_tmp, kb.d, c->d_s_m, c->d_s_can, c->d_s2_m, c->d_pmod, total, (int)L,
+       (int)c->logn, c->P.seed, kid, c->special_id, c->d_mods);
+    CHECK_LAUNCH();
+    c->keys[kid] = kb;
+    c->key_bytes += words * 8;
+    *out = kb.d;
+    return 0;
+}
+
+extern "C" int fhe_keygen_rotations(fhe_ctx *c, const uint32_t *steps, uint32_t m) {
+    for (u32 i = 0; i < m; i++) {
+        if (steps[i] == 0 || steps[i] >= c->N) return fail(FHE_EINVAL, "rotation step %u outside [1, %u)", steps[i], c->N);
+        const u64 *k;
+        TRY(get_key(c, galois_elt(c, steps[i]), &k));
+    }
+    return 0;
+}
+
+// ================================================================== objects
+extern "C" int fhe_ct_create(fhe_ctx *c, uint32_t R, uint32_t level, fhe_ct **out) {
+    if (R < 1) return fail(FHE_EINVAL, "R must be >= 1");
+    if (level < 1 || level > c->L) return fail(FHE_ELEVEL, "level %u outside [1, %u]", level, c->L);
+    fhe_ct *ct = new fhe_ct{c, R, level, R * c->T, nullptr};
+    cudaError_t e = cudaMallocAsync((void **)&ct->d, ct_words(ct) * 8, c->st);
+    if (e != cudaSuccess) {
+        delete ct;
+        return fail(FHE_ENOMEM, "ciphertext allocation of %zu bytes failed: %s", (size_t)R * c->T * 2 * level * c->n * 8,
+                    cudaGetErrorString(e));
+    }
+    *out = ct;
+    return 0;
+}
+extern "C" void fhe_ct_destroy(fhe_ct *ct) {
+    if (!ct) return;
+    cudaFreeAsync(ct->d, ct->ctx->st);
+    delete ct;
+}
+extern "C" uint32_t fhe_ct_level(const fhe_ct *ct) { return ct->level; }
+extern "C" uint32_t fhe_ct_rows(const fhe_ct *ct) { return ct->R; }
+
+extern "C" int fhe_ct_read(fhe_ctx *c, const fhe_ct *ct, uint64_t *w) {
+    CU(cudaMemcpyAsync(w, ct->d, ct_words(ct) * 8, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+extern "C" int fhe_ct_write(fhe_ctx *c, fhe_ct *ct, const uint64_t *w) {
+    CU(cudaMemcpyAsync(ct->d, w, ct_words(ct) * 8, cudaMemcpyHostToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+extern "C" int fhe_ct_zero(fhe_ctx *c, fhe_ct *ct) {
+    CU(cudaMemsetAsync(ct->d, 0, ct_words(ct) * 8, c->st));
+    return 0;
+}
+
+extern "C" int fhe_pt_create(fhe_ctx *c, fhe_pt **out) {
+    fhe_pt *pt = new fhe_pt{c, nullptr, nullptr, 0};
+    size_t n = c->n;
+    if (cudaMallocAsync((void **)&pt->coef_t, c->T * n * 8, c->st) != cudaSuccess ||
+        cudaMallocAsync((void **)&pt->ntt_m, (size_t)c->T * c->L * n * 8, c->st) != cudaSuccess) {
+        delete pt;
+        return fail(FHE_ENOMEM, "plaintext allocation failed");
+    }
+    *out = pt;
+    return 0;
+}
+extern "C" void fhe_pt_destroy(fhe_pt *pt) {
+    if (!pt) return;
+    cudaFreeAsync(pt->coef_t, pt->ctx->st);
+    cudaFreeAsync(pt->ntt_m, pt->ctx->st);
+    delete pt;
+}
+
+// slots [rows][n] (device) -> coefficients mod t_{(r / div) % T} (device)
+static int slots_to_coef(fhe_ctx *c, const u64 *slots, u64 *coef, int rows, u32 div) {
+    InttRowsArgs a = iargs(slots, coef, c->n);
+    a.div = div;
+    a.period = c->T;
+    map_range(a.map, c->T, c->t_id0);
+    a.gather = 1;
+    a.tab = c->d_ntt2slot;
+    a.reduce = 1;
+    return intt_rows(c, rows, a);
+}
+
+extern "C" int fhe_encode(fhe_ctx *c, const uint64_t *slots, fhe_pt *pt) {
+    size_t n = c->n;
+    TRY(ensure_tmp(c, c->T * n));
+    CU(cudaMemcpyAsync(c->w_tmp, slots, c->T * n * 8, cudaMemcpyHostToDevice, c->st));
+    TRY(slots_to_coef(c, c->w_tmp, pt->coef_t, (int)c->T, 1));
+    // centered lift t_k -> q_i, NTT, Montgomery form; row r = k*L + i
+    NttRowsArgs a = nargs(pt->coef_t, pt->ntt_m, 0);
+    a.rdiv = c->L; a.sA = n; a.sB = 0; a.dA = (long long)c->L * n; a.dB = n;
+    a.div = 1; a.period = c->L; map_q(a.map, c->L);
+    a.div2 = c->L; a.period2 = c->T; map_range(a.srcmap, c->T, c->t_id0);
+    a.load = 2; a.epi = 1;
+    TRY(ntt_rows(c, (int)(c->T * c->L), a));
+    // the host buffer must outlive the copy
+    CU(cudaStreamSynchronize(c->st));
+    pt->encoded = 1;
+    return 0;
+}
+
+extern "C" int fhe_pt_read(fhe_ctx *c, const fhe_pt *pt, uint64_t *w) {
+    size_t words = (size_t)c->T * c->L * c->n;
+    TRY(ensure_tmp(c, words));
+    EW(k_from_mont, (long long)words, pt->ntt_m, c->w_tmp, (long long)words, (int)c->L, (int)c->logn, c->d_mods);
+    CHECK_LAUNCH();
+    CU(cudaMemcpyAsync(w, c->w_tmp, words * 8, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+// ============================================================ client side
+extern "C" int fhe_encrypt(fhe_ctx *c, const uint64_t *slots, uint32_t nonce, fhe_ct *ct) {
+    if (ct->level != c->L) return fail(FHE_ELEVEL, "encryption target must be at the top level");
+    size_t n = c->n, L = c->L, cnt = ct->count;
+    TRY(ensure_tmp(c, cnt * n * (2 + L)));
+    u64 *s_dev = c->w_tmp, *m = c->w_tmp + cnt * n, *tmp = m + cnt * n;
+    CU(cudaMemcpyAsync(s_dev, slots, cnt * n * 8, cudaMemcpyHostToDevice, c->st));
+    TRY(slots_to_coef(c, s_dev, m, (int)cnt, ct->R));
+    long long total = (long long)cnt * L * n;
+    EW(k_enc_prep, total, m, tmp, total, (int)L, (int)ct->R, (int)c->logn, c->P.seed, nonce, c->d_lv + L, c->t_id0,
+       c->d_mods);
+    CHECK_LAUNCH();
+    NttRowsArgs a = nargs(tmp, tmp, n);
+    a.period = L;
+    map_q(a.map, L);
+    TRY(ntt_rows(c, (int)(cnt * L), a));
+    EW(k_enc_finish, total, tmp, ct->d, c->d_s_m, total, (int)L, (int)c->logn, c->P.seed, nonce, c->d_mods);
+    CHECK_LAUNCH();
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+// x = INTT(c0 + c1 s) into dst [count][l][n]
+static int raw_decrypt(fhe_ctx *c, const fhe_ct *ct, u64 *dst) {
+    size_t n = c->n, l = ct->level;
+    long long total = (long long)ct->count * l * n;
+    EW(k_dec_mul, total, ct->d, c->d_s_m, dst, total, (int)l, (int)c->logn, c->d_mods);
+    CHECK_LAUNCH();
+    InttRowsArgs a = iargs(dst, dst, n);
+    a.period = l;
+    map_q(a.map, l);
+    return intt_rows(c, (int)(ct->count * l), a);
+}
+
+extern "C" int fhe_decrypt(fhe_ctx *c, const fhe_ct *ct, uint64_t *slots) {
+    size_t n = c->n, l = ct->level, cnt = ct->count;
+    TRY(ensure_tmp(c, cnt * n * (l + 2)));
+    u64 *X = c->w_tmp, *m = X + cnt * l * n, *o = m + cnt * n;
+    TRY(raw_decrypt(c, ct, X));
+    long long total = (long long)cnt * n;
+    EW(k_dec_scale, total, X, m, total, (int)l, (int)ct->R, (int)c->logn, c->d_lv + l, c->t_id0, c->d_mods);
+    CHECK_LAUNCH();
+    NttRowsArgs a = nargs(m, m, n);
+    a.div = ct->R;
+    a.period = c->T;
+    map_range(a.map, c->T, c->t_id0);
+    TRY(ntt_rows(c, (int)cnt, a));
+    EW(k_gather_slots, total, m, o, total, (int)c->logn, c->d_slot2ntt);
+    CHECK_LAUNCH();
+    CU(cudaMemcpyAsync(slots, o, cnt * n * 8, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+extern "C" int fhe_decrypt_raw(fhe_ctx *c, const fhe_ct *ct, uint64_t *out) {
+    size_t words = (size_t)ct->count * ct->level * c->n;
+    TRY(ensure_tmp(c, words));
+    TRY(raw_decrypt(c, ct, c->w_tmp));
+    CU(cudaMemcpyAsync(out, c->w_tmp, words * 8, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+// =============================================================== evaluation
+static bool same_shape(const fhe_ct *a, const fhe_ct *b) { return a->R == b->R && a->level == b->level; }
+
+extern "C" int fhe_add(fhe_ctx *c, const fhe_ct *a, const fhe_ct *b, fhe_ct *out) {
+    if (!same_shape(a, b) || !same_shape(a, out)) return fail(FHE_ELEVEL, "add: shape/level mismatch");
+    long long total = (long long)ct_words(a);
+    EW(k_add, total, a->d, b->d, out->d, total, (int)a->level, (int)c->logn, c->d_mods);
+    CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int fhe_mul_plain(fhe_ctx *c, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out) {
+    if (!same_shape(a, out)) return fail(FHE_ELEVEL, "mul_plain: shape/level mismatch");
+    if (!pt->encoded) return fail(FHE_EINVAL, "mul_plain: plaintext was never encoded");
+    long long total = (long long)ct_words(a);
+    EW(k_mul_plain, total, a->d, pt->ntt_m, out->d, total, (int)a->level, (int)c->L, (int)a->R, (int)c->logn,
+       c->d_mods);
+    CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int fhe_mul_scalar(fhe_ctx *c, const fhe_ct *a, int64_t w, fhe_ct *out) {
+    if (!same_shape(a, out)) return fail(FHE_ELEVEL, "mul_scalar: shape/level mismatch");
+    ScalarTab st;
+    memset(&st, 0, sizeof st);
+    for (u32 i = 0; i < a->level; i++) {
+        u64 q = c->P.q[i];
+        u64 v = w >= 0 ? (u64)w % q : hm::neg((u64)(-(w + 1)) % q + 1, q);
+        st.w[i] = v;
+        st.wsh[i] = hm::shoup(v, q);
+    }
+    long long total = (long long)ct_words(a);
+    EW(k_mul_scalar, total, a->d, out->d, total, (int)a->level, (int)c->logn, st, c->d_mods);
+    CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int fhe_add_plain(fhe_ctx *c, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out) {
+    if (!same_shape(a, out)) return fail(FHE_ELEVEL, "add_plain: shape/level mismatch");
+    if (!pt->encoded) return fail(FHE_EINVAL, "add_plain: plaintext was never encoded");
+    size_t n = c->n, l = a->level;
+    TRY(ensure_tmp(c, c->T * l * n));
+    long long total = (long long)c->T * l * n;
+    EW(k_scaled_msg, total, pt->coef_t, c->w_tmp, total, (int)l, 1, (int)c->logn, c->d_lv + l, c->t_id0, c->d_mods);
+    CHECK_LAUNCH();
+    NttRowsArgs na = nargs(c->w_tmp, c->w_tmp, n);
+    na.period = l;
+    map_q(na.map, l);
+    TRY(ntt_rows(c, (int)(c->T * l), na));
+    long long tw = (long long)ct_words(a);
+    EW(k_add_pt, tw, a->d, c->w_tmp, out->d, tw, (int)l, (int)a->R, (int)c->logn, c->d_mods);
+    CHECK_LAUNCH();
+    return 0;
+}
+
+// ---------------------------------------------------------- key switching
+// Digits of S cts: dt.coef[s] + j n (coefficient form), dt.ntt[s] + j n (NTT
+// form).  Result: out[s][p][i] = ModDown(sum_j digit_j * key_j)[p][i] + add[s][p][i].
+struct KsOut {
+    u64 *out[MAXS];
+    const u64 *add[MAXS];
+    long long out_pstride, add_pstride;
+    int add_pmask;
+};
+
+static int keyswitch_core(fhe_ctx *c, int S, u32 l, const u64 *key, const DigitTab &dt, const KsOut &ko) {
+    size_t n = c->n;
+    int L = (int)c->L;
+    // ModUp: every off-diagonal (digit, prime) pair
+    LOGN_SWITCH(c->logn, launch_row<LG>(k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
+                                        c->d_mods));
+    CHECK_LAUNCH();
+    long long tot = (long long)(l + 1) * n;
+    k_ks_inner<<<(unsigned)nblocks(tot), 256, 0, c->st>>>(c->w_Ext, dt, key, c->w_Acc, S, (int)l, L, (int)c->logn,
+                                                           c->special_id, c->d_mods);
+    CHECK_LAUNCH();
+    // ModDown: INTT of the special limb of both accumulators
+    InttRowsArgs ia = iargs(c->w_Acc + l * n, c->w_Acc + l * n, (long long)(l + 1) * n);
+    ia.map.id[0] = (unsigned char)c->special_id;
+    TRY(intt_rows(c, 2 * S, ia));
+    RescaleArgs ra;
+    memset(&ra, 0, sizeof ra);
+    for (int s = 0; s < S; s++) {
+        ra.coef[s] = c->w_Acc + ((size_t)s * 2 * (l + 1) + l) * n;
+        ra.base[s] = c->w_Acc + (size_t)s * 2 * (l + 1) * n;
+        ra.out[s] = ko.out[s];
+        ra.add[s] = ko.add[s];
+    }
+    ra.coef_pstride = (long long)(l + 1) * n;
+    ra.base_pstride = (long long)(l + 1) * n;
+    ra.out_pstride = ko.out_pstride;
+    ra.add_pstride = ko.add_pstride;
+    ra.add_pmask = ko.add_pmask;
+    ra.src_id = c->special_id;
+    for (u32 i = 0; i < l; i++) { ra.fac[i] = c->pinv[i]; ra.fac_sh[i] = c->pinv_sh[i]; }
+    LOGN_SWITCH(c->logn, launch_row<LG>(k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
+    CHECK_LAUNCH();
+    return 0;
+}
+
+// rotate a list of physical ciphertexts (each [2][l][n]) by Galois element g
+static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std::vector<u64 *> &out, u32 l, u32 g) {
+    const u64 *key;
+    TRY(get_key(c, g, &key));
+    size_t n = c->n;
+    for (size_t b0 = 0; b0 < in.size(); b0 += c->S) {
+        int S = (int)std::min<size_t>(c->S, in.size() - b0);
+        PtrTab pt;
+        memset(&pt, 0, sizeof pt);
+        for (int s = 0; s < S; s++) { pt.in[s] = in[b0 + s]; pt.out[s] = out[b0 + s]; }
+        LOGN_SWITCH(c->logn, launch_row<LG>(k_rot_gather_intt<LG>, dim3(S, 2, l), c->st, pt, (int)l, g, c->w_C0,
+                                            c->w_C1, c->w_D, c->d_mods));
+        CHECK_LAUNCH();
+        DigitTab dt;
+        KsOut ko;
+        memset(&dt, 0, sizeof dt);
+        memset(&ko, 0, sizeof ko);
+        for (int s = 0; s < S; s++) {
+            dt.coef[s] = c->w_D + (size_t)s * l * n;
+            dt.ntt[s] = c->w_C1 + (size_t)s * l * n;
+            ko.out[s] = out[b0 + s];
+            ko.add[s] = c->w_C0 + (size_t)s * l * n;
+        }
+        ko.out_pstride = (long long)l * n;
+        ko.add_pstride = 0;
+        ko.add_pmask = 1;
+        TRY(keyswitch_core(c, S, l, key, dt, ko));
+    }
+    return 0;
+}
+
+static int check_rot(fhe_ctx *c, u32 k) {
+    if (k == 0 || k >= c->N) return fail(FHE_EINVAL, "rotation step %u outside [1, %u)", k, c->N);
+    return 0;
+}
+
+extern "C" int fhe_rotate(fhe_ctx *c, const fhe_ct *a, uint32_t k, fhe_ct *out) {
+    TRY(check_rot(c, k));
+    if (!same_shape(a, out)) return fail(FHE_ELEVEL, "rotate: shape/level mismatch");
+    if (a == out || a->d == out->d) return fail(FHE_EINVAL, "rotate: out must not alias the input");
+    std::vector<const u64 *> in;
+    std::vector<u64 *> o;
+    size_t stride = 2ull * a->level * c->n;
+    for (u32 ci = 0; ci < a->count; ci++) { in.push_back(a->d + ci * stride); o.push_back(out->d + ci * stride); }
+    return rotate_phys(c, in, o, a->level, galois_elt(c, k));
+}
+
+extern "C" int fhe_rotate_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k) {
+    TRY(check_rot(c, k));
+    if (!m) return 0;
+    u32 l = a[0]->level;
+    std::vector<const u64 *> in;
+    std::vector<u64 *> o;
+    for (u32 h = 0; h < m; h++) {
+        if (a[h]->level != l || !same_shape(a[h], out[h])) return fail(FHE_ELEVEL, "rotate_many: shape/level mismatch");
+        if (a[h]->d == out[h]->d) return fail(FHE_EINVAL, "rotate_many: out must not alias the input");
+        size_t stride = 2ull * l * c->n;
+        for (u32 ci = 0; ci < a[h]->count; ci++) { in.push_back(a[h]->d + ci * stride); o.push_back(out[h]->d + ci * stride); }
+    }
+    return rotate_phys(c, in, o, l, galois_elt(c, k));
+}
+
+extern "C" int fhe_mul_plain_many(fhe_ctx *c, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m) {
+    for (u32 i = 0; i < m; i++) TRY(fhe_mul_plain(c, a[i], pt[i], out[i]));
+    return 0;
+}
+extern "C" int fhe_add_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *b, fhe_ct *const *out, uint32_t m) {
+    for (u32 i = 0; i < m; i++) TRY(fhe_add(c, a[i], b[i], out[i]));
+    return 0;
+}
+
+// ------------------------------------------------------------ mod switch
+extern "C" int fhe_mod_switch(fhe_ctx *c, const fhe_ct *a, fhe_ct *out) {
+    u32 l = a->level;
+    size_t n = c->n;
+    if (l < 2) return fail(FHE_ELEVEL, "mod_switch: already at level 1");
+    if (out->level != l - 1 || out->R != a->R) return fail(FHE_ELEVEL, "mod_switch: out must have level %u", l - 1);
+    size_t cnt = a->count;
+    TRY(ensure_tmp(c, cnt * 2 * n));
+    // INTT of the dropped limb of both polynomials: row r = ci*2 + p
+    InttRowsArgs ia = iargs(a->d + (l - 1) * n, c->w_tmp, (long long)l * n);
+    ia.dA = n;
+    ia.map.id[0] = (unsigned char)(l - 1);
+    TRY(intt_rows(c, (int)(cnt * 2), ia));
+    const LevelDev &T = c->hlv[l];
+    for (size_t b0 = 0; b0 < cnt; b0 += MAXS) {
+        int S = (int)std::min<size_t>(MAXS, cnt - b0);
+        RescaleArgs ra;
+        memset(&ra, 0, sizeof ra);
+        for (int s = 0; s < S; s++) {
+            size_t ci = b0 + s;
+            ra.coef[s] = c->w_tmp + ci * 2 * n;
+            ra.base[s] = a->d + ci * 2 * l * n;
+            ra.out[s] = out->d + ci * 2 * (l - 1) * n;
+        }
+        ra.coef_pstride = n;
+        ra.base_pstride = (long long)l * n;
+        ra.out_pstride = (long long)(l - 1) * n;
+        ra.src_id = (int)(l - 1);
+        for (u32 i = 0; i + 1 < l; i++) { ra.fac[i] = T.msinv[i]; ra.fac_sh[i] = T.msinv_sh[i]; }
+        LOGN_SWITCH(c->logn, launch_row<LG>(k_rescale<LG>, dim3(S, 2, l - 1), c->st, ra, c->d_mods));
+        CHECK_LAUNCH();
+    }
+    return 0;
+}
+
+// --------------------------------------------------------------- squaring
+extern "C" int fhe_square(fhe_ctx *c, const fhe_ct *a, fhe_ct *out) {
+    if (!c->nb) return fail(FHE_EINVAL, "square: context created without an auxiliary base");
+    if (!same_shape(a, out)) return fail(FHE_ELEVEL, "square: shape/level mismatch");
+    if (a == out || a->d == out->d) return fail(FHE_EINVAL, "square: out must not alias the input");
+    const u64 *rk;
+    TRY(get_key(c, 0, &rk));
+    size_t n = c->n, l = a->level, nb = c->nb, nt = l + nb;
+    const size_t per = n * (2 * l + 2 * nb + 3 * nt + 3 * l + 3 * l);
+    int Smax = (int)std::min<size_t>(c->S, c->w_sq_words / per);
+    if (Smax < 1) return fail(FHE_ENOMEM, "square workspace too small");
+    for (size_t b0 = 0; b0 < a->count; b0 += Smax) {
+        int S = (int)std::min<size_t>(Smax, a->count - b0);
+        const u64 *in = a->d + b0 * 2 * l * n;
+        u64 *X = c->w_sq, *Xb = X + S * 2 * l * n, *D = Xb + S * 2 * nb * n, *E = D + S * 3 * nt * n,
+            *En = E + S * 3 * l * n;
+        // 1. coefficient form of c0, c1 over Q_l
+        InttRowsArgs ia = iargs(in, X, n);
+        ia.period = l;
+        map_q(ia.map, l);
+        TRY(intt_rows(c, S * 2 * (int)l, ia));
+        // 2. centered lift to B, NTT over B
+        long long tot = (long long)S * 2 * n;
+        EW(k_sq_lift, tot, X, Xb, tot, (int)l, (int)nb, (int)c->logn, c->d_lv + l, c->b_id0, c->d_mods);
+        CHECK_LAUNCH();
+        NttRowsArgs na = nargs(Xb, Xb, n);
+        na.period = nb;
+        map_range(na.map, nb, c->b_id0);
+        TRY(ntt_rows(c, S * 2 * (int)nb, na));
+        // 3. tensor over Q_l u B, back to coefficients
+        tot = (long long)S * nt * n;
+        EW(k_sq_tensor, tot, in, Xb, D, tot, (int)l, (int)nb, (int)c->logn, c->b_id0, c->d_mods);
+        CHECK_LAUNCH();
+        ia = iargs(D, D, n);
+        ia.period = nt;
+        for (size_t ii = 0; ii < nt; ii++) ia.map.id[ii] = (unsigned char)(ii < l ? ii : c->b_id0 + ii - l);
+        TRY(intt_rows(c, S * 3 * (int)nt, ia));
+        // 4. scale by t/Q_l into B, back to Q_l
+        tot = (long long)S * 3 * n;
+        EW(k_sq_scale, tot, D, E, tot, (int)l, (int)nb, (int)a->R, (int)b0, (int)c->logn, c->d_lv + l, c->d_ax,
+           c->b_id0, c->d_mods);
+        CHECK_LAUNCH();
+        na = nargs(E, En, n);
+        na.period = l;
+        map_q(na.map, l);
+        TRY(ntt_rows(c, S * 3 * (int)l, na));
+        // 5. relinearize e2, add e0/e1
+        DigitTab dt;
+        KsOut ko;
+        memset(&dt, 0, sizeof dt);
+        memset(&ko, 0, sizeof ko);
+        for (int s = 0; s < S; s++) {
+            dt.coef[s] = E + ((size_t)s * 3 + 2) * l * n;
+            dt.ntt[s] = En + ((size_t)s * 3 + 2) * l * n;
+            ko.out[s] = out->d + (b0 + s) * 2 * l * n;
+            ko.add[s] = En + (size_t)s * 3 * l * n;
+        }
+        ko.out_pstride = (long long)l * n;
+        ko.add_pstride = (long long)l * n;
+        ko.add_pmask = 3;
+        TRY(keyswitch_core(c, S, (u32)l, rk, dt, ko));
+    }
+    return 0;
+}

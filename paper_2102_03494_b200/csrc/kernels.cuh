@@ -1,0 +1,614 @@
+// kernels.cuh -- sm_100a kernels of the packed RNS-BFV evaluator.
+//
+// Row kernels (one polynomial row of n words per CTA, templated on log2 n) fuse
+// their loads (automorphism gather, cross-prime reduction, centered lift) and
+// epilogues (Montgomery conversion, ModDown / mod-switch combine) around the
+// shared-memory NTT cores.  Elementwise kernels are grid-stride loops over
+// 64-bit words with coalesced, limb-major access.
+#pragma once
+#include "ntt_core.cuh"
+
+#define MAXQ 24
+#define MAXB 26
+#define MAXT 8
+#define MAXS 64   // physical ciphertexts per key-switching sub-batch
+
+struct LevelDev {
+    // decryption / encryption (per plaintext modulus k)
+    u64 Qtilde_m[MAXQ];            // (Q_l/q_i)^-1 mod q_i, Montgomery form
+    u64 decW[MAXT][MAXQ];
+    u64 decFhi[MAXT][MAXQ], decFlo[MAXT][MAXQ];
+    u64 delta_m[MAXT][MAXQ];       // floor(Q_l/t_k) mod q_i, Montgomery form
+    u64 rt[MAXT];                  // Q_l mod t_k
+    u64 rtF[MAXT];                 // floor(rt 2^64 / t_k)
+    u64 msinv[MAXQ], msinv_sh[MAXQ];   // q_{l-1}^-1 mod q_i (Shoup)
+    u64 half_last;                 // (q_{l-1}-1)/2
+    u64 qlast_mod[MAXQ];           // q_{l-1} mod q_i
+    // squaring
+    u64 invq_hi[MAXQ], invq_lo[MAXQ];
+    u64 QhatB_m[MAXQ][MAXB];
+    u64 QmodB_m[MAXB];
+    u64 Mtq_m[MAXQ];
+    u64 Mtb_m[MAXB];
+    u64 omega_m[MAXT][MAXQ][MAXB];
+    u64 theta_hi[MAXT][MAXQ], theta_lo[MAXT][MAXQ];
+    u64 tBb_m[MAXT][MAXB];
+};
+
+struct AuxDev {
+    u64 Btilde_m[MAXB];
+    u64 invb_hi[MAXB], invb_lo[MAXB];
+    u64 BhatQ_m[MAXB][MAXQ];
+    u64 BmodQ_m[MAXQ];
+};
+
+struct ModMap {
+    unsigned char id[64];
+};
+
+// ============================================================== row kernels
+
+// Forward NTT of rows.  Row r: src + r*sstride, dst + r*dstride; modulus
+// mods[map.id[(r / div) % period]].
+//   load 0: plain (< 4q)   1: reduce any 64-bit word   2: centered lift from
+//           source modulus srcmap (values in [0, m_src))
+//   epi  0: store canonical   1: store Montgomery form   2: dst += v
+struct NttRowsArgs {
+    const u64 *src;
+    u64 *dst;
+    u32 rdiv;                      // row r -> (r / rdiv, r % rdiv)
+    long long sA, sB, dA, dB;      // src/dst word offsets per coordinate
+    u32 div, period;               // modulus: map.id[(r / div) % period]
+    u32 div2, period2;             // source modulus: srcmap.id[(r / div2) % period2]
+    ModMap map, srcmap;
+    int load, epi;
+};
+DEV long long row_off(int r, u32 rdiv, long long A, long long B) { return (long long)(r / rdiv) * A + (long long)(r % rdiv) * B; }
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_ntt_rows(NttRowsArgs a, const ModInfo *__restrict__ mods) {
+    using C = NttCfg<LOGN>;
+    extern __shared__ u64 sm[];
+    const int r = blockIdx.x, tid = threadIdx.x;
+    const ModInfo M = mods[a.map.id[(r / a.div) % a.period]];
+    const u64 *src = a.src + row_off(r, a.rdiv, a.sA, a.sB);
+    u64 v[C::E];
+    u64 half_src = 0, msrc_q = 0;
+    if (a.load == 2) {
+        const ModInfo &S = mods[a.srcmap.id[(r / a.div2) % a.period2]];
+        half_src = S.half;
+        msrc_q = red64(S.q, M.q, M.mu);
+    }
+#pragma unroll
+    for (int e = 0; e < C::E; e++) {
+        u64 x = src[(e << (LOGN - C::W)) | tid];
+        if (a.load == 1) x = red64(x, M.q, M.mu);
+        else if (a.load == 2) x = centered_lift(x, half_src, msrc_q, M);
+        v[e] = x;
+    }
+    ntt_fwd_core<LOGN>(v, sm, M, tid);
+    u64 *dst = a.dst + row_off(r, a.rdiv, a.dA, a.dB);
+    for (int i = tid; i < C::N; i += C::TH) {
+        u64 x = sm[spad(i)];
+        if (a.epi == 1) x = to_mont(x, M);
+        else if (a.epi == 2) x = addm(dst[i], x, M.q);
+        dst[i] = x;
+    }
+}
+
+// Inverse NTT of rows, optional gather on load:
+//   gather 0: none   1: src[tab[j]] (slot -> NTT position)   2: automorphism by g
+struct InttRowsArgs {
+    const u64 *src;
+    u64 *dst;
+    u32 rdiv;
+    long long sA, sB, dA, dB;
+    u32 div, period;
+    ModMap map;
+    int gather;
+    const u32 *tab;
+    u32 g;
+    int reduce;   // 1: reduce inputs mod q first (values may exceed q)
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_intt_rows(InttRowsArgs a, const ModInfo *__restrict__ mods) {
+    using C = NttCfg<LOGN>;
+    extern __shared__ u64 sm[];
+    const int r = blockIdx.x, tid = threadIdx.x;
+    const ModInfo M = mods[a.map.id[(r / a.div) % a.period]];
+    const u64 *src = a.src + row_off(r, a.rdiv, a.sA, a.sB);
+    if (a.gather == 2) {
+        for (int i = tid; i < C::N; i += C::TH) sm[spad(i)] = src[i];
+        __syncthreads();
+        u64 w[C::E];
+#pragma unroll
+        for (int e = 0; e < C::E; e++) w[e] = sm[spad(galois_perm(tid + e * C::TH, a.g, LOGN))];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < C::E; e++) sm[spad(tid + e * C::TH)] = w[e];
+    } else {
+        for (int i = tid; i < C::N; i += C::TH) {
+            u64 x = a.gather == 1 ? src[a.tab[i]] : src[i];
+            if (a.reduce) x = red64(x, M.q, M.mu);
+            sm[spad(i)] = x;
+        }
+    }
+    __syncthreads();
+    u64 v[C::E];
+    ntt_inv_core<LOGN>(v, sm, M, tid);
+    u64 *dst = a.dst + row_off(r, a.rdiv, a.dA, a.dB);
+#pragma unroll
+    for (int e = 0; e < C::E; e++) dst[(e << (LOGN - C::W)) | tid] = v[e];
+}
+
+struct PtrTab {
+    const u64 *in[MAXS];
+    u64 *out[MAXS];
+};
+
+// Key switching, step 1 (rotation).  grid (S, 2, l): row (s, p, i) of input
+// ciphertext s.  c0 rows: permuted copy -> C0p[s][i].  c1 rows: permuted copy ->
+// C1p[s][i] (NTT form of digit i, used on the inner-product diagonal), INTT -> D[s][i].
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt, int l, u32 g, u64 *C0p, u64 *C1p,
+                                                                  u64 *D, const ModInfo *__restrict__ mods) {
+    using C = NttCfg<LOGN>;
+    extern __shared__ u64 sm[];
+    const int s = blockIdx.x, p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
+    const long long n = C::N;
+    const u64 *src = pt.in[s] + ((long long)p * l + i) * n;
+    for (int x = tid; x < C::N; x += C::TH) sm[spad(x)] = src[x];
+    __syncthreads();
+    u64 w[C::E];
+#pragma unroll
+    for (int e = 0; e < C::E; e++) w[e] = sm[spad(galois_perm(tid + e * C::TH, g, LOGN))];
+    u64 *side = (p == 0 ? C0p : C1p) + ((long long)s * l + i) * n;
+#pragma unroll
+    for (int e = 0; e < C::E; e++) side[tid + e * C::TH] = w[e];
+    if (p == 0) return;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < C::E; e++) sm[spad(tid + e * C::TH)] = w[e];
+    __syncthreads();
+    const ModInfo M = mods[i];
+    u64 v[C::E];
+    ntt_inv_core<LOGN>(v, sm, M, tid);
+    u64 *dst = D + ((long long)s * l + i) * n;
+#pragma unroll
+    for (int e = 0; e < C::E; e++) dst[(e << (LOGN - C::W)) | tid] = v[e];
+}
+
+struct DigitTab {
+    const u64 *coef[MAXS];   // digit j of ct s at coef[s] + j*n (coefficient form, < q_j)
+    const u64 *ntt[MAXS];    // the same digits in NTT form (inner-product diagonal)
+};
+
+// Key switching, step 2 (ModUp).  grid (S, l, l+1): digit j of ct s reduced into
+// prime i (i == l: the special prime) and transformed; the diagonal i == j is
+// skipped (the inner product reads it from DigitTab.ntt).
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
+                                                        const ModInfo *__restrict__ mods) {
+    using C = NttCfg<LOGN>;
+    extern __shared__ u64 sm[];
+    const int s = blockIdx.x, j = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
+    if (i == j) return;
+    const long long n = C::N;
+    const ModInfo M = mods[i == l ? special_id : i];
+    const u64 *src = dt.coef[s] + j * n;
+    u64 v[C::E];
+#pragma unroll
+    for (int e = 0; e < C::E; e++) v[e] = red64(src[(e << (LOGN - C::W)) | tid], M.q, M.mu);
+    ntt_fwd_core<LOGN>(v, sm, M, tid);
+    u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n;
+    for (int x = tid; x < C::N; x += C::TH) dst[x] = sm[spad(x)];
+}
+
+// Rescale by a dropped prime (ModDown over the special prime, or BFV modulus
+// switching over q_{l-1}).  grid (S, 2, l_out): row (s, p, i)
+//   r   = coef[s] + p*coef_pstride              (coefficient form mod m_src)
+//   out = (base[s][p][i] - NTT_i(centered r)) * fac_i  (+ addend[s][p][i])
+struct RescaleArgs {
+    const u64 *coef[MAXS];
+    const u64 *base[MAXS];
+    u64 *out[MAXS];
+    const u64 *add[MAXS];         // nullable per s
+    long long coef_pstride, base_pstride, out_pstride, add_pstride;
+    int add_pmask;                // bit p set: add addend for output poly p
+    int src_id;                   // modulus id of the dropped prime
+    u64 fac[MAXQ], fac_sh[MAXQ];
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
+    using C = NttCfg<LOGN>;
+    extern __shared__ u64 sm[];
+    const int s = blockIdx.x, p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
+    const long long n = C::N;
+    const ModInfo M = mods[i];
+    const ModInfo &S = mods[a.src_id];
+    const u64 half_src = S.half, msrc_q = red64(S.q, M.q, M.mu);
+    const u64 *r = a.coef[s] + p * a.coef_pstride;
+    u64 v[C::E];
+#pragma unroll
+    for (int e = 0; e < C::E; e++) v[e] = centered_lift(r[(e << (LOGN - C::W)) | tid], half_src, msrc_q, M);
+    ntt_fwd_core<LOGN>(v, sm, M, tid);
+    const u64 *base = a.base[s] + p * a.base_pstride + i * n;
+    u64 *out = a.out[s] + p * a.out_pstride + i * n;
+    const u64 *add = ((a.add_pmask >> p) & 1) && a.add[s] ? a.add[s] + p * a.add_pstride + i * n : nullptr;
+    const u64 f = a.fac[i], fsh = a.fac_sh[i];
+    for (int x = tid; x < C::N; x += C::TH) {
+        u64 y = shoup(subm(base[x], sm[spad(x)], M.q) , f, fsh, M.q);
+        if (add) y = addm(y, add[x], M.q);
+        out[x] = y;
+    }
+}
+
+// ========================================================= elementwise kernels
+
+#define GRID_STRIDE(i, total) \
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (total); i += (long long)gridDim.x * blockDim.x)
+
+// Key switching, step 3: acc_p[s][i] = sum_j Ext[s][j][i] * key_p[j][i]; keys in
+// Montgomery form, layout [L digits][2][L+1 primes][n].  One thread per (i, x),
+// looping the sub-batch so each key word is loaded once.
+__global__ void k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, const u64 *__restrict__ key,
+                           u64 *__restrict__ Acc, int S, int l, int L, int logn, int special_id,
+                           const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, (long long)(l + 1) * n) {
+        const int i = (int)(idx >> logn);
+        const long long x = idx & (n - 1);
+        const int kp = i == l ? L : i;
+        const ModInfo &M = mods[i == l ? special_id : i];
+        const u64 q = M.q, qi = M.qinv;
+        for (int s0 = 0; s0 < S; s0 += 4) {
+            u64 a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
+            const int sc = S - s0 < 4 ? S - s0 : 4;
+            for (int j = 0; j < l; j++) {
+                const u64 kb = __ldg(key + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
+                const u64 ka = __ldg(key + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    if (u < sc) {
+                        const u64 e = i == j ? dt.ntt[s0 + u][(long long)j * n + x]
+                                             : Ext[((((long long)(s0 + u) * l + j) * (l + 1)) + i) * n + x];
+                        a0[u] = addm(a0[u], mont(e, kb, q, qi), q);
+                        a1[u] = addm(a1[u], mont(e, ka, q, qi), q);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                if (u < sc) {
+                    Acc[(((long long)(s0 + u) * 2 + 0) * (l + 1) + i) * n + x] = a0[u];
+                    Acc[(((long long)(s0 + u) * 2 + 1) * (l + 1) + i) * n + x] = a1[u];
+                }
+            }
+        }
+    }
+}
+
+// out = a + b over [count][2][l][n]
+__global__ void k_add(const u64 *__restrict__ a, const u64 *__restrict__ b, u64 *__restrict__ out, long long total,
+                      int l, int logn, const ModInfo *__restrict__ mods) {
+    GRID_STRIDE(idx, total) {
+        const int i = (int)((idx >> logn) % l);
+        out[idx] = addm(a[idx], b[idx], mods[i].q);
+    }
+}
+
+// out[ci][p][i] = a[ci][p][i] * pt[k][i] (pt Montgomery form, k = ci / R)
+__global__ void k_mul_plain(const u64 *__restrict__ a, const u64 *__restrict__ ptm, u64 *__restrict__ out,
+                            long long total, int l, int L, int R, int logn, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;
+        const int i = (int)(row % l);
+        const long long ci = row / (2 * l);
+        const int k = (int)(ci / R);
+        const ModInfo &M = mods[i];
+        const u64 w = __ldg(ptm + ((long long)k * L + i) * n + (idx & (n - 1)));
+        out[idx] = mont(a[idx], w, M.q, M.qinv);
+    }
+}
+
+struct ScalarTab {
+    u64 w[MAXQ], wsh[MAXQ];
+};
+__global__ void k_mul_scalar(const u64 *__restrict__ a, u64 *__restrict__ out, long long total, int l, int logn,
+                             ScalarTab st, const ModInfo *__restrict__ mods) {
+    GRID_STRIDE(idx, total) {
+        const int i = (int)((idx >> logn) % l);
+        out[idx] = shoup(a[idx], st.w[i], st.wsh[i], mods[i].q);
+    }
+}
+
+// round(Q_l m / t_k) mod q_i for a coefficient m in [0, t_k):
+// Delta*m + round(rt*m/t) with Delta = floor(Q_l/t_k), rt = Q_l mod t_k.
+DEV u64 scaled_msg(const LevelDev &T, int k, u64 t, u64 m, int i, const ModInfo &Mq) {
+    const u64 rt = T.rt[k];
+    u64 est = mulhi(m, T.rtF[k]);                        // floor(rt m / t) - {0,1}
+    u128 rem = (u128)rt * m - (u128)est * t;
+    while (rem >= t) { rem -= t; est++; }
+    const u64 corr = est + (2 * (u64)rem >= t ? 1 : 0);
+    return addm(mont(red64(m, Mq.q, Mq.mu), T.delta_m[k][i], Mq.q, Mq.qinv), red64(corr, Mq.q, Mq.mu), Mq.q);
+}
+
+// rows [count][l][n] (or [T][l][n] with R = 1): out = NTT-pending scaled message
+// m: [T][n] coefficient rows mod t_k (ct row ci uses m[ci / R])
+__global__ void k_scaled_msg(const u64 *__restrict__ m, u64 *__restrict__ out, long long total, int l, int R,
+                             int logn, const LevelDev *__restrict__ T, int t_id0, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;
+        const int i = (int)(row % l);
+        const int k = (int)(row / l / R);
+        const long long x = idx & (n - 1);
+        out[idx] = scaled_msg(*T, k, mods[t_id0 + k].q, m[(row / l) * n + x], i, mods[i]);
+    }
+}
+
+// encryption, before the NTT: tmp[ci][i] = e_ci mod q_i + round(Q m / t)
+__global__ void k_enc_prep(const u64 *__restrict__ m, u64 *__restrict__ tmp, long long total, int L, int R,
+                           int logn, u64 seed, u32 nonce, const LevelDev *__restrict__ T, int t_id0,
+                           const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;                 // ci * L + i
+        const int i = (int)(row % L);
+        const u32 ci = (u32)(row / L);
+        const int k = (int)(ci / R);
+        const u32 x = (u32)(idx & (n - 1));
+        const ModInfo &M = mods[i];
+        const int e = sample_cbd(seed, DOM_ENC_E, 0, nonce, ci, x);
+        const u64 sm_ = scaled_msg(*T, k, mods[t_id0 + k].q, m[(long long)ci * n + x], i, M);
+        tmp[idx] = addm(smod(e, M), sm_, M.q);
+    }
+}
+
+// encryption, after the NTT: c1 = a (uniform, NTT domain), c0 = tmp - a*s
+__global__ void k_enc_finish(const u64 *__restrict__ tmp, u64 *__restrict__ ct, const u64 *__restrict__ s_m,
+                             long long total, int L, int logn, u64 seed, u32 nonce, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;
+        const int i = (int)(row % L);
+        const u32 ci = (u32)(row / L);
+        const u32 x = (u32)(idx & (n - 1));
+        const ModInfo &M = mods[i];
+        const u64 a = sample_uniform(M, seed, DOM_ENC_A, i, nonce, ci, x);
+        const u64 as = mont(a, s_m[(long long)i * n + x], M.q, M.qinv);
+        u64 *c = ct + ((long long)ci * 2 * L) * n;
+        c[((long long)0 * L + i) * n + x] = subm(tmp[idx], as, M.q);
+        c[((long long)1 * L + i) * n + x] = a;
+    }
+}
+
+// decryption: x = c0 + c1 * s over [count][l][n]
+__global__ void k_dec_mul(const u64 *__restrict__ ct, const u64 *__restrict__ s_m, u64 *__restrict__ out,
+                          long long total, int l, int logn, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;
+        const int i = (int)(row % l);
+        const long long ci = row / l;
+        const long long x = idx & (n - 1);
+        const ModInfo &M = mods[i];
+        const u64 *c = ct + ci * 2 * l * n;
+        const u64 c0 = c[(long long)i * n + x], c1 = c[((long long)l + i) * n + x];
+        out[idx] = addm(c0, mont(c1, s_m[(long long)i * n + x], M.q, M.qinv), M.q);
+    }
+}
+
+// decryption: per coefficient m = round(t x / Q_l) mod t via the fixed-point sum
+__global__ void k_dec_scale(const u64 *__restrict__ X, u64 *__restrict__ m, long long total, int l, int R, int logn,
+                            const LevelDev *__restrict__ T, int t_id0, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long ci = idx >> logn;
+        const long long x = idx & (n - 1);
+        const int k = (int)(ci / R);
+        u128 ai = 0, af = 0;
+        for (int i = 0; i < l; i++) {
+            const ModInfo &M = mods[i];
+            const u64 y = mont(X[(ci * l + i) * n + x], T->Qtilde_m[i], M.q, M.qinv);
+            fx_acc(ai, af, y, T->decW[k][i], T->decFhi[k][i], T->decFlo[k][i]);
+        }
+        m[idx] = mod128(ai + (af >> 127), mods[t_id0 + k]);
+    }
+}
+
+// out[ci][x] = A[ci][slot2ntt[x]]
+__global__ void k_gather_slots(const u64 *__restrict__ A, u64 *__restrict__ out, long long total, int logn,
+                               const u32 *__restrict__ slot2ntt) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long ci = idx >> logn;
+        out[idx] = A[ci * n + slot2ntt[idx & (n - 1)]];
+    }
+}
+
+// secret key: per prime id row, ternary s mod q (NTT pending)
+__global__ void k_sk_prep(u64 *__restrict__ out, long long total, int logn, u64 seed, const unsigned char *ids,
+                          const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const int r = (int)(idx >> logn);
+        const u32 x = (u32)(idx & (n - 1));
+        out[idx] = smod(sample_ternary(seed, DOM_SK, 0, 0, 0, x), mods[ids[r]]);
+    }
+}
+
+// key generation, before the NTT: rows [L digits][L+1 primes]: e_j mod prime
+__global__ void k_key_prep(u64 *__restrict__ out, long long total, int L, int logn, u64 seed, u32 kid,
+                           int special_id, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;
+        const int i = (int)(row % (L + 1));
+        const u32 j = (u32)(row / (L + 1));
+        const u32 x = (u32)(idx & (n - 1));
+        out[idx] = smod(sample_cbd(seed, DOM_KSK_E, j, kid, 0, x), mods[i == L ? special_id : i]);
+    }
+}
+
+// key generation, after the NTT: key[j][0][i] = e - a s + [i == j] P target,
+// key[j][1][i] = a, both stored in Montgomery form.  target = s^2 (kid 0) or
+// s(X^kid), from the canonical NTT-domain secret.
+__global__ void k_key_finish(const u64 *__restrict__ e_ntt, u64 *__restrict__ key, const u64 *__restrict__ s_m,
+                             const u64 *__restrict__ s_can, const u64 *__restrict__ s2_m, const u64 *__restrict__ pmod,
+                             long long total, int L, int logn, u64 seed, u32 kid, int special_id,
+                             const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;
+        const int i = (int)(row % (L + 1));
+        const int j = (int)(row / (L + 1));
+        const u32 x = (u32)(idx & (n - 1));
+        const ModInfo &M = mods[i == L ? special_id : i];
+        const u64 a = sample_uniform(M, seed, DOM_KSK_A, (u32)(j * 64 + i), kid, 0, x);
+        u64 b = subm(e_ntt[idx], mont(a, s_m[(long long)i * n + x], M.q, M.qinv), M.q);
+        if (i == j) {
+            u64 tgt;
+            if (kid == 0) tgt = mont(s2_m[(long long)i * n + x], 1, M.q, M.qinv);   // canonical s^2
+            else tgt = s_can[(long long)i * n + galois_perm(x, kid, logn)];
+            b = addm(b, mulmod(pmod[i], tgt, M), M.q);
+        }
+        key[(((long long)j * 2 + 0) * (L + 1) + i) * n + x] = to_mont(b, M);
+        key[(((long long)j * 2 + 1) * (L + 1) + i) * n + x] = to_mont(a, M);
+    }
+}
+
+// ---------------------------------------------------------------- squaring
+// lift: X[ci][p][0..l) coefficient rows over Q_l -> Xb[ci][p][k] over B (centered)
+__global__ void k_sq_lift(const u64 *__restrict__ X, u64 *__restrict__ Xb, long long total, int l, int nb,
+                          int logn, const LevelDev *__restrict__ T, int b_id0, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;          // ci * 2 + p
+        const long long x = idx & (n - 1);
+        u64 y[MAXQ];
+        u128 ai = 0, af = 0;
+        for (int i = 0; i < l; i++) {
+            const ModInfo &M = mods[i];
+            y[i] = mont(X[(row * l + i) * n + x], T->Qtilde_m[i], M.q, M.qinv);
+            fx_acc(ai, af, y[i], 0, T->invq_hi[i], T->invq_lo[i]);
+        }
+        const u64 v = (u64)(ai + (af >> 127));
+        for (int k = 0; k < nb; k++) {
+            const ModInfo &B = mods[b_id0 + k];
+            u64 s = 0;
+            for (int i = 0; i < l; i++) s = addm(s, mont(y[i], T->QhatB_m[i][k], B.q, B.qinv), B.q);
+            s = subm(s, mont(red64(v, B.q, B.mu), T->QmodB_m[k], B.q, B.qinv), B.q);
+            Xb[(row * nb + k) * n + x] = s;
+        }
+    }
+}
+
+// tensor in NTT domain over Q_l u B.  Xq: the input ct [ci][2][l], Xb: [ci][2][nb];
+// D: [ci][3][l + nb]
+__global__ void k_sq_tensor(const u64 *__restrict__ Xq, const u64 *__restrict__ Xb, u64 *__restrict__ D,
+                            long long total, int l, int nb, int logn, int b_id0, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    const int nt = l + nb;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;          // ci * nt + ii
+        const int ii = (int)(row % nt);
+        const long long ci = row / nt;
+        const long long x = idx & (n - 1);
+        const ModInfo &M = mods[ii < l ? ii : b_id0 + ii - l];
+        u64 a0, a1;
+        if (ii < l) {
+            a0 = Xq[((ci * 2 + 0) * l + ii) * n + x];
+            a1 = Xq[((ci * 2 + 1) * l + ii) * n + x];
+        } else {
+            a0 = Xb[((ci * 2 + 0) * nb + ii - l) * n + x];
+            a1 = Xb[((ci * 2 + 1) * nb + ii - l) * n + x];
+        }
+        const u64 d0 = mulmod(a0, a0, M), m01 = mulmod(a0, a1, M), d2 = mulmod(a1, a1, M);
+        D[((ci * 3 + 0) * nt + ii) * n + x] = d0;
+        D[((ci * 3 + 1) * nt + ii) * n + x] = addm(m01, m01, M.q);
+        D[((ci * 3 + 2) * nt + ii) * n + x] = d2;
+    }
+}
+
+// scale: D coefficient rows over Q_l u B -> E[ci][3][l] = round(t/Q_l d) over Q_l
+__global__ void k_sq_scale(const u64 *__restrict__ D, u64 *__restrict__ E, long long total, int l, int nb, int R,
+                           int ci0, int logn, const LevelDev *__restrict__ T, const AuxDev *__restrict__ A, int b_id0,
+                           const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    const int nt = l + nb;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;          // ci * 3 + p
+        const long long ci = row / 3;
+        const int kt = (int)((ci + ci0) / R);
+        const long long x = idx & (n - 1);
+        const u64 *Dp = D + row * nt * n;
+        u64 y[MAXQ];
+        u128 ai = 0, af = 0;
+        for (int i = 0; i < l; i++) {
+            const ModInfo &M = mods[i];
+            y[i] = mont(Dp[(long long)i * n + x], T->Mtq_m[i], M.q, M.qinv);
+            fx_acc(ai, af, y[i], 0, T->theta_hi[kt][i], T->theta_lo[kt][i]);
+        }
+        const u128 rnd = ai + (af >> 127);
+        u64 yb[MAXB];
+        u128 bi = 0, bf = 0;
+        for (int k = 0; k < nb; k++) {
+            const ModInfo &B = mods[b_id0 + k];
+            u64 s = mod128(rnd, B);
+            for (int i = 0; i < l; i++) s = addm(s, mont(y[i], T->omega_m[kt][i][k], B.q, B.qinv), B.q);
+            const u64 z = mont(Dp[(long long)(l + k) * n + x], T->Mtb_m[k], B.q, B.qinv);
+            s = addm(s, mont(z, T->tBb_m[kt][k], B.q, B.qinv), B.q);
+            yb[k] = mont(s, A->Btilde_m[k], B.q, B.qinv);
+            fx_acc(bi, bf, yb[k], 0, A->invb_hi[k], A->invb_lo[k]);
+        }
+        const u64 v = (u64)(bi + (bf >> 127));
+        for (int i = 0; i < l; i++) {
+            const ModInfo &M = mods[i];
+            u64 s = 0;
+            for (int k = 0; k < nb; k++) s = addm(s, mont(yb[k], A->BhatQ_m[k][i], M.q, M.qinv), M.q);
+            s = subm(s, mont(red64(v, M.q, M.mu), A->BmodQ_m[i], M.q, M.qinv), M.q);
+            E[(row * l + i) * n + x] = s;
+        }
+    }
+}
+
+// add_plain: out[ci][0][i] = a[ci][0][i] + tmp[ci / R][i]; c1 copied
+__global__ void k_add_pt(const u64 *__restrict__ a, const u64 *__restrict__ tmp, u64 *__restrict__ out,
+                         long long total, int l, int R, int logn, const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    GRID_STRIDE(idx, total) {
+        const long long row = idx >> logn;          // (ci * 2 + p) * l + i
+        const int i = (int)(row % l);
+        const int p = (int)((row / l) & 1);
+        const long long ci = row / (2 * l);
+        u64 v = a[idx];
+        if (p == 0) v = addm(v, tmp[((ci / R) * l + i) * n + (idx & (n - 1))], mods[i].q);
+        out[idx] = v;
+    }
+}
+
+// secret key after the NTT: Montgomery copies of s and s^2
+__global__ void k_sk_finish(const u64 *__restrict__ s_can, u64 *__restrict__ s_m, u64 *__restrict__ s2_m,
+                            long long total, int n_s2_rows, int logn, const unsigned char *ids,
+                            const ModInfo *__restrict__ mods) {
+    GRID_STRIDE(idx, total) {
+        const int r = (int)(idx >> logn);
+        const ModInfo &M = mods[ids[r]];
+        const u64 s = s_can[idx];
+        s_m[idx] = to_mont(s, M);
+        if (r < n_s2_rows) s2_m[idx] = to_mont(mulmod(s, s, M), M);
+    }
+}
+
+// Montgomery -> canonical (plaintext readback)
+__global__ void k_from_mont(const u64 *__restrict__ in, u64 *__restrict__ out, long long total, int L, int logn,
+                            const ModInfo *__restrict__ mods) {
+    GRID_STRIDE(idx, total) {
+        const ModInfo &M = mods[(int)((idx >> logn) % L)];
+        out[idx] = mont(in[idx], 1, M.q, M.qinv);
+    }
+}

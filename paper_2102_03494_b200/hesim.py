@@ -1,0 +1,512 @@
+"""Reference-facing slot API, backed by the sm_100a RNS-BFV evaluator.
+
+Mirrors `cipherpack.hesim` (/root/reference/pkg/src/cipherpack/hesim.py) name for
+name: `SchemeParams`, `OpCounters`, `PlainVector`, `SlotCiphertext`, `HeContext`,
+`rotations_for_span`, `merge_contexts` and the three error types, with the same
+argument meaning, counter/depth semantics and error behaviour.  What changes is
+underneath: a tracked `SlotCiphertext` holds a device handle to real BFV
+ciphertexts instead of a numpy slot array.
+
+Differences a caller can observe, all deliberate:
+
+* one context evaluates `batch` images at once; every primitive acts on all of
+  them (images 2r and 2r+1 share the two batching rows of row-pair r);
+* `encrypt`/`decrypt` accept/return one slot vector per image when batch > 1;
+* `ct.slots` is a decrypting property (test convenience, costs a decrypt);
+* the `rotate_and_sum` zero-tail precondition needs a decrypt, so it is only
+  checked when the context was built with `debug_checks=True`;
+* t must factor into primes = 1 mod 2N (SIMD batching); a composite t is given
+  through `SchemeParams.t_factors` and evaluated by plaintext CRT.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .params import RlweParams, batching_compatible, make_params
+
+_INT64_T_LIMIT = 1 << 62
+
+
+class CapacityError(ValueError):
+    """Payload does not fit into the available slots."""
+
+
+class EncodingOverflowError(ValueError):
+    """A signed value falls outside the representable range (-t/2, t/2)."""
+
+
+class PreconditionError(ValueError):
+    """An operation's slot-content precondition is violated."""
+
+
+@dataclass(frozen=True)
+class SchemeParams:
+    """Slot count N and plaintext modulus t (reference: hesim.py:61-95).
+
+    t_factors optionally lists the prime factorization of t used for plaintext
+    CRT; rlwe optionally pins the full RNS-BFV parameter set.
+    """
+
+    n_slots: int
+    t: int
+    rotation_weight: float = 10.0
+    noise_budget_bits: int | None = None
+    security_bits: int | None = None
+    t_factors: tuple | None = None
+    rlwe: RlweParams | None = field(default=None, compare=False)
+
+    def __post_init__(self):
+        if self.n_slots < 2 or (self.n_slots & (self.n_slots - 1)) != 0:
+            raise ValueError(f"n_slots must be a power of two >= 2, got {self.n_slots}")
+        if self.t < 2:
+            raise ValueError(f"plaintext modulus must be >= 2, got {self.t}")
+        if not self.rotation_weight > 0:
+            raise ValueError("rotation_weight must be positive")
+        if self.t_factors is not None:
+            object.__setattr__(self, "t_factors", tuple(int(f) for f in self.t_factors))
+            if math.prod(self.t_factors) != self.t:
+                raise ValueError("t_factors do not multiply to t")
+
+    @property
+    def int64_storage(self) -> bool:
+        return self.t <= _INT64_T_LIMIT
+
+    @property
+    def max_value(self) -> int:
+        return (self.t - 1) // 2
+
+    def factors(self) -> tuple[int, ...]:
+        if self.t_factors is not None:
+            return self.t_factors
+        return (self.t,)
+
+
+@dataclass
+class OpCounters:
+    """Additive tallies of homomorphic operations (reference: hesim.py:97-134)."""
+
+    mul_pc: int = 0
+    add_cc: int = 0
+    rot: int = 0
+    mul_cc: int = 0
+    assembly_mul_pc: int = 0
+
+    def copy(self) -> "OpCounters":
+        return replace(self)
+
+    def __sub__(self, other: "OpCounters") -> "OpCounters":
+        return OpCounters(*(getattr(self, f) - getattr(other, f) for f in _FIELDS))
+
+    def __add__(self, other: "OpCounters") -> "OpCounters":
+        return OpCounters(*(getattr(self, f) + getattr(other, f) for f in _FIELDS))
+
+    def merge(self, other: "OpCounters") -> None:
+        for f in _FIELDS:
+            setattr(self, f, getattr(self, f) + getattr(other, f))
+
+
+_FIELDS = ("mul_pc", "add_cc", "rot", "mul_cc", "assembly_mul_pc")
+
+
+class PlainVector:
+    """Unencrypted slot vector, canonical residues in [0, t) (hesim.py:137-151).
+
+    The device encoding is created on first use and cached by content.
+    """
+
+    __slots__ = ("slots", "params", "_key")
+
+    def __init__(self, slots: np.ndarray, params: SchemeParams):
+        self.slots = slots
+        self.params = params
+        self._key = None
+
+    def centered(self) -> np.ndarray:
+        lift = (self.params.t + 1) // 2
+        out = self.slots.astype(np.int64, copy=True) if self.params.int64_storage else self.slots.copy()
+        out[self.slots >= lift] -= self.params.t
+        return out
+
+    def content_key(self) -> bytes:
+        if self._key is None:
+            arr = np.asarray(self.slots)
+            if arr.dtype == object:
+                arr = np.array([str(int(v)) for v in arr]).astype("S")
+            self._key = hashlib.blake2b(arr.tobytes(), digest_size=16).digest()
+        return self._key
+
+
+class SlotCiphertext:
+    """Packed ciphertext: device handle plus depth counters (hesim.py:154-171).
+
+    `handle is None` marks a count-only ciphertext.
+    """
+
+    __slots__ = ("handle", "depth", "params", "assembly_depth", "_ctx")
+
+    def __init__(self, handle, depth: int, params: SchemeParams, assembly_depth: int = 0, ctx=None):
+        self.handle = handle
+        self.depth = depth
+        self.params = params
+        self.assembly_depth = assembly_depth
+        self._ctx = ctx
+
+    @property
+    def tracked(self) -> bool:
+        return self.handle is not None
+
+    @property
+    def slots(self):
+        """Residues in [0, t) (decrypts; test/debug convenience)."""
+        if self.handle is None:
+            return None
+        return self._ctx._residues(self)
+
+    @property
+    def level(self) -> int:
+        return self.handle.level
+
+
+def rotations_for_span(m: int) -> int:
+    """ceil(log2 m): rotate-and-sum cost over an m-slot payload (hesim.py:369-373)."""
+    if m < 1:
+        raise ValueError("span must be positive")
+    return (m - 1).bit_length()
+
+
+def default_rlwe(params: SchemeParams, levels: int | None = None, q_bits: int | None = None) -> RlweParams:
+    """RNS-BFV parameters for a SchemeParams."""
+    if params.rlwe is not None:
+        return params.rlwe
+    factors = params.factors()
+    for f in factors:
+        if not batching_compatible(f, params.n_slots):
+            raise ValueError(
+                f"plaintext modulus factor {f} does not admit SIMD batching over {params.n_slots} slots "
+                f"(needs a prime = 1 mod {4 * params.n_slots} below 2^61); pass t_factors or rlwe")
+    qb = q_bits or (55 if params.n_slots >= 1024 else 50)
+    return make_params(params.n_slots, factors, levels=levels or 4, q_bits=qb)
+
+
+class HeContext:
+    """One evaluation context: scheme parameters, counters, and a GPU evaluator.
+
+    batch: images evaluated by every call (two per batching-row pair).
+    lib:   the ABI implementation; default is the CUDA build (raises if absent).
+    """
+
+    def __init__(self, params: SchemeParams, *, batch: int = 1, lib=None, levels: int | None = None,
+                 q_bits: int | None = None, debug_checks: bool = False, pt_cache: bool = True):
+        if batch < 1:
+            raise ValueError("batch must be >= 1")
+        self.params = params
+        self.counters = OpCounters()
+        self.elided_rotations = 0
+        self.batch = batch
+        self.rows = (batch + 1) // 2
+        self.debug_checks = debug_checks
+        self._lib = lib
+        self._levels = levels
+        self._q_bits = q_bits
+        self._ev = None
+        self._pt_cache = {} if pt_cache else None
+
+    # ------------------------------------------------------------------ device
+    @property
+    def evaluator(self):
+        if self._ev is None:
+            from .rlwe import Evaluator
+            rp = default_rlwe(self.params, self._levels, self._q_bits)
+            if rp.n_slots != self.params.n_slots:
+                raise ValueError("rlwe parameters do not match n_slots")
+            self._ev = Evaluator(rp, self._lib)
+        return self._ev
+
+    def _wrap(self, handle, depth, assembly_depth=0) -> SlotCiphertext:
+        return SlotCiphertext(handle, depth, self.params, assembly_depth, ctx=self)
+
+    def _factor_residues(self, values: np.ndarray) -> np.ndarray:
+        """signed ints (..., k) -> uint64 residues (T, ..., k)"""
+        fs = self.evaluator.params.t
+        if values.dtype != object and values.size and np.max(np.abs(values.astype(np.float64))) < 2 ** 62:
+            v = values.astype(np.int64)
+            return np.stack([np.mod(v, f).astype(np.uint64) for f in fs])
+        v = values.astype(object)
+        return np.stack([np.array((v % f).tolist(), dtype=np.uint64).reshape(v.shape) for f in fs])
+
+    def _layout(self, per_image: np.ndarray) -> np.ndarray:
+        """(T, batch, N) residues -> (T, R, 2N) row-pair layout."""
+        T, B, N = per_image.shape
+        out = np.zeros((T, self.rows, 2 * N), dtype=np.uint64)
+        out[:, :, :N] = per_image[:, 0::2]
+        if B > 1:
+            out[:, : B // 2, N:] = per_image[:, 1::2]
+        return out
+
+    def _device_pt(self, pv: PlainVector):
+        key = pv.content_key()
+        if self._pt_cache is not None and key in self._pt_cache:
+            return self._pt_cache[key]
+        N = self.params.n_slots
+        res = self._factor_residues(np.asarray(pv.centered()))          # (T, N)
+        both = np.concatenate([res, res], axis=1)                        # replicate to row 1
+        pt = self.evaluator.encode(both)
+        if self._pt_cache is not None:
+            self._pt_cache[key] = pt
+        return pt
+
+    def _residues(self, ct: SlotCiphertext):
+        """Decrypted residues mod t, (N,) for batch 1 else (batch, N)."""
+        ev = self.evaluator
+        raw = ev.decrypt(ct.handle)                                      # (T, R, 2N) uint64
+        N = self.params.n_slots
+        per = np.empty((raw.shape[0], self.batch, N), dtype=np.uint64)
+        per[:, 0::2] = raw[:, : (self.batch + 1) // 2, :N]
+        if self.batch > 1:
+            per[:, 1::2] = raw[:, : self.batch // 2, N:]
+        fs = ev.params.t
+        if len(fs) == 1:
+            out = per[0].astype(np.int64) if self.params.int64_storage else per[0].astype(object)
+        else:
+            t = self.params.t
+            acc = np.zeros(per.shape[1:], dtype=object)
+            for f, r in zip(fs, per):
+                mf = t // f
+                acc = acc + r.astype(object) * (mf * pow(mf, -1, f))
+            acc = acc % t
+            out = acc.astype(np.int64) if self.params.int64_storage else acc
+        return out[0] if self.batch == 1 else out
+
+    # --------------------------------------------------------------- client
+    def encode(self, values) -> PlainVector:
+        """Encode signed integers into a plaintext slot vector (hesim.py:203-215)."""
+        values = np.asarray(values)
+        n, t = self.params.n_slots, self.params.t
+        if values.size > n:
+            raise CapacityError(f"{values.size} values exceed {n} slots")
+        flat = values.ravel()
+        if flat.size and int(2 * np.max(np.abs(flat.astype(object)))) >= t:
+            raise EncodingOverflowError(f"|value| must be < t/2 = {t / 2}")
+        dtype = np.int64 if self.params.int64_storage else object
+        slots = np.zeros(n, dtype=dtype)
+        if flat.size:
+            res = np.asarray(flat, dtype=object) % t
+            slots[: flat.size] = res.astype(np.int64) if self.params.int64_storage else res
+        return PlainVector(slots, self.params)
+
+    def encrypt(self, values) -> SlotCiphertext:
+        """One slot vector for every image ((k,)), or one per image ((batch, k))."""
+        values = np.asarray(values)
+        n, t = self.params.n_slots, self.params.t
+        per_image = values.ndim == 2
+        if per_image and values.shape[0] != self.batch:
+            raise ValueError(f"expected {self.batch} slot vectors, got {values.shape[0]}")
+        k = values.shape[-1] if values.ndim else values.size
+        if k > n:
+            raise CapacityError(f"{k} values exceed {n} slots")
+        if values.size and int(2 * np.max(np.abs(values.astype(object)))) >= t:
+            raise EncodingOverflowError(f"|value| must be < t/2 = {t / 2}")
+        mat = np.zeros((self.batch, n), dtype=values.dtype if values.dtype != object else object)
+        if per_image:
+            mat[:, :k] = values
+        elif values.size:
+            mat[:, :k] = values.ravel()[None, :]
+        res = self._factor_residues(mat)                                  # (T, batch, N)
+        handle = self.evaluator.encrypt(self._layout(res))
+        return self._wrap(handle, 0)
+
+    def encrypt_zero(self, tracked: bool = True) -> SlotCiphertext:
+        if not tracked:
+            return SlotCiphertext(None, 0, self.params)
+        return self._wrap(self.evaluator.zero(self.rows), 0)
+
+    def encrypt_untracked(self) -> SlotCiphertext:
+        return SlotCiphertext(None, 0, self.params)
+
+    def decrypt(self, ct: SlotCiphertext) -> np.ndarray:
+        """Centered representatives in [-t/2, t/2), object array (hesim.py:231-238)."""
+        if not ct.tracked:
+            raise ValueError("cannot decrypt a count-only ciphertext")
+        t = self.params.t
+        res = np.asarray(self._residues(ct)).astype(object)
+        res[res >= (t + 1) // 2] -= t
+        return res
+
+    def noise_budget(self, ct: SlotCiphertext) -> float:
+        """Minimum remaining invariant-noise budget (bits) over all physical cts."""
+        return float(np.min(self.evaluator.noise_budget(ct.handle)))
+
+    # ----------------------------------------------------------- primitives
+    def _align(self, a: SlotCiphertext, b: SlotCiphertext):
+        """Bring two tracked cts to the same level (mod switch the higher)."""
+        ha, hb = a.handle, b.handle
+        while ha.level > hb.level:
+            ha = self.evaluator.mod_switch(ha)
+        while hb.level > ha.level:
+            hb = self.evaluator.mod_switch(hb)
+        return ha, hb
+
+    def rotate(self, ct: SlotCiphertext, k: int, charge_identity: bool = False) -> SlotCiphertext:
+        """Cyclic left rotation: output slot i = input slot (i+k) mod N (hesim.py:244-261)."""
+        n = self.params.n_slots
+        if not 0 <= k < n:
+            raise ValueError(f"rotation amount must be in [0, {n}), got {k}")
+        if k != 0 or charge_identity:
+            self.counters.rot += 1
+        if k == 0:
+            if not charge_identity:
+                self.elided_rotations += 1
+            return ct
+        if not ct.tracked:
+            return SlotCiphertext(None, ct.depth, ct.params, ct.assembly_depth)
+        return self._wrap(self.evaluator.rotate(ct.handle, k), ct.depth, ct.assembly_depth)
+
+    def mul_plain(self, ct: SlotCiphertext, pv: PlainVector | None, assembly: bool = False) -> SlotCiphertext:
+        """Slot-wise product mod t; one multiplicative level (hesim.py:263-283)."""
+        if assembly:
+            self.counters.assembly_mul_pc += 1
+        else:
+            self.counters.mul_pc += 1
+        depth = ct.depth + (0 if assembly else 1)
+        adepth = ct.assembly_depth + (1 if assembly else 0)
+        if not ct.tracked:
+            return SlotCiphertext(None, depth, ct.params, adepth)
+        if pv is None:
+            raise ValueError("tracked ciphertext requires a plaintext operand")
+        out = self.evaluator.mul_plain(ct.handle, self._device_pt(pv))
+        return self._wrap(out, depth, adepth)
+
+    def mul_scalar(self, ct: SlotCiphertext, w: int) -> SlotCiphertext:
+        """mul_plain by the constant-w plaintext, valid when every slot outside the
+        constant's support is zero (ConvPacked columns, packing.py:96-98); tallied
+        as one mul_pc like the reference's masked-constant multiply (engine.py:192-193)."""
+        self.counters.mul_pc += 1
+        depth = ct.depth + 1
+        if not ct.tracked:
+            return SlotCiphertext(None, depth, ct.params, ct.assembly_depth)
+        return self._wrap(self.evaluator.mul_scalar(ct.handle, int(w)), depth, ct.assembly_depth)
+
+    def add_cc(self, a: SlotCiphertext, b: SlotCiphertext) -> SlotCiphertext:
+        """Slot-wise sum mod t; depth is the max of the operands (hesim.py:304-316)."""
+        if a.params != b.params:
+            raise ValueError("ciphertexts come from different schemes")
+        self.counters.add_cc += 1
+        depth = max(a.depth, b.depth)
+        adepth = max(a.assembly_depth, b.assembly_depth)
+        if not (a.tracked and b.tracked):
+            return SlotCiphertext(None, depth, a.params, adepth)
+        ha, hb = self._align(a, b)
+        return self._wrap(self.evaluator.add(ha, hb), depth, adepth)
+
+    def add_plain(self, ct: SlotCiphertext, pv: PlainVector | None) -> SlotCiphertext:
+        """Plaintext addition; uncounted (hesim.py:318-326)."""
+        if not ct.tracked:
+            return ct
+        if pv is None:
+            raise ValueError("tracked ciphertext requires a plaintext operand")
+        out = self.evaluator.add_plain(ct.handle, self._device_pt(pv))
+        return self._wrap(out, ct.depth, ct.assembly_depth)
+
+    def square(self, ct: SlotCiphertext) -> SlotCiphertext:
+        """Slot-wise square mod t (ct x ct multiply + relinearization) (hesim.py:328-345)."""
+        self.counters.mul_cc += 1
+        depth = ct.depth + 1
+        if not ct.tracked:
+            return SlotCiphertext(None, depth, ct.params, ct.assembly_depth)
+        return self._wrap(self.evaluator.square(ct.handle), depth, ct.assembly_depth)
+
+    def mod_switch(self, ct: SlotCiphertext) -> SlotCiphertext:
+        """BFV modulus switch (drop one prime); no reference counterpart, uncounted."""
+        if not ct.tracked:
+            return ct
+        return self._wrap(self.evaluator.mod_switch(ct.handle), ct.depth, ct.assembly_depth)
+
+    def rotate_and_sum(self, ct: SlotCiphertext, m: int) -> SlotCiphertext:
+        """slot 0 <- sum of the first m slots; ceil(log2 m) rotations/additions (hesim.py:347-366)."""
+        return self.rotate_and_sum_many([ct], m)[0]
+
+    # --------------------------------------------------- batched primitives
+    # Same counters and results as issuing the calls one by one; the device
+    # work of each list is one launch sequence.
+    def mul_plain_many(self, cts, pvs, assembly: bool = False):
+        cts = list(cts)
+        pvs = list(pvs)
+        if assembly:
+            self.counters.assembly_mul_pc += len(cts)
+        else:
+            self.counters.mul_pc += len(cts)
+        tracked = [c.tracked for c in cts]
+        if not any(tracked):
+            return [SlotCiphertext(None, c.depth + (0 if assembly else 1), c.params,
+                                   c.assembly_depth + (1 if assembly else 0)) for c in cts]
+        if not all(tracked):
+            raise ValueError("mixed tracked/untracked operands")
+        if any(p is None for p in pvs):
+            raise ValueError("tracked ciphertext requires a plaintext operand")
+        outs = self.evaluator.mul_plain_many([c.handle for c in cts], [self._device_pt(p) for p in pvs])
+        return [self._wrap(o, c.depth + (0 if assembly else 1), c.assembly_depth + (1 if assembly else 0))
+                for o, c in zip(outs, cts)]
+
+    def rotate_many(self, cts, k: int):
+        cts = list(cts)
+        n = self.params.n_slots
+        if not 0 <= k < n:
+            raise ValueError(f"rotation amount must be in [0, {n}), got {k}")
+        if k == 0:
+            self.elided_rotations += len(cts)
+            return cts
+        self.counters.rot += len(cts)
+        if not cts[0].tracked:
+            return [SlotCiphertext(None, c.depth, c.params, c.assembly_depth) for c in cts]
+        groups: dict[int, list[int]] = {}
+        for i, c in enumerate(cts):
+            groups.setdefault(c.handle.level, []).append(i)
+        outs = [None] * len(cts)
+        for idx in groups.values():
+            res = self.evaluator.rotate_many([cts[i].handle for i in idx], k)
+            for i, h in zip(idx, res):
+                outs[i] = self._wrap(h, cts[i].depth, cts[i].assembly_depth)
+        return outs
+
+    def add_cc_many(self, a, b):
+        a, b = list(a), list(b)
+        self.counters.add_cc += len(a)
+        if not a[0].tracked:
+            return [SlotCiphertext(None, max(x.depth, y.depth), x.params, max(x.assembly_depth, y.assembly_depth))
+                    for x, y in zip(a, b)]
+        pairs = [self._align(x, y) for x, y in zip(a, b)]
+        outs = self.evaluator.add_many([p[0] for p in pairs], [p[1] for p in pairs])
+        return [self._wrap(o, max(x.depth, y.depth), max(x.assembly_depth, y.assembly_depth))
+                for o, x, y in zip(outs, a, b)]
+
+    def rotate_and_sum_many(self, cts, m: int):
+        n = self.params.n_slots
+        if not 1 <= m <= n:
+            raise ValueError(f"m must be in [1, {n}], got {m}")
+        cts = list(cts)
+        if self.debug_checks and m < n:
+            for ct in cts:
+                if ct.tracked:
+                    res = np.asarray(self._residues(ct))
+                    if np.any(res[..., m:]):
+                        raise PreconditionError(f"slots at index >= {m} must be zero")
+        rounds = (m - 1).bit_length()
+        acc = cts
+        for h in reversed(range(rounds)):
+            acc = self.add_cc_many(acc, self.rotate_many(acc, 1 << h))
+        return acc
+
+
+def merge_contexts(target: HeContext, *others: HeContext) -> HeContext:
+    """Fold counters of per-thread contexts into one (hesim.py:376-383)."""
+    for other in others:
+        if other.params != target.params:
+            raise ValueError("contexts use different scheme parameters")
+        target.counters.merge(other.counters)
+        target.elided_rotations += other.elided_rotations
+    return target
