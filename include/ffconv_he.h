@@ -79,6 +79,17 @@ void fhe_ctx_destroy(fhe_ctx *ctx);
 int fhe_sync(fhe_ctx *ctx);
 /* bytes of device (or host, golden) memory held by keys and tables */
 int fhe_ctx_key_bytes(fhe_ctx *ctx, uint64_t *out);
+/* the context's CUDA stream (cudaStream_t), for event timing by the caller */
+int fhe_ctx_stream(fhe_ctx *ctx, void **stream);
+/* measured integer-pipe roofline: chained 64-bit Shoup modular multiplications
+ * per second over the whole GPU (register resident, all SMs) */
+int fhe_peak_modmul(fhe_ctx *ctx, uint32_t iters, double *modmul_per_s);
+/* per-kernel CUDA-event profiling: when enabled, every launch is bracketed by
+ * events; fhe_prof_report syncs and writes "name calls total_ms\n" lines
+ * (then clears).  fhe_launch_count: kernels launched since creation. */
+int fhe_prof_enable(fhe_ctx *ctx, int on);
+int fhe_prof_report(fhe_ctx *ctx, char *buf, uint32_t len);
+int fhe_launch_count(fhe_ctx *ctx, uint64_t *out);
 /* generate Galois keys for the given rotation steps now (otherwise lazily) */
 int fhe_keygen_rotations(fhe_ctx *ctx, const uint32_t *steps, uint32_t m);
 

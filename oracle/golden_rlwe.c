@@ -517,6 +517,14 @@ void fhe_ctx_destroy(fhe_ctx *c) {
 }
 
 int fhe_sync(fhe_ctx *ctx) { (void)ctx; return 0; }
+int fhe_ctx_stream(fhe_ctx *ctx, void **stream) { (void)ctx; *stream = NULL; return 0; }
+int fhe_prof_enable(fhe_ctx *ctx, int on) { (void)ctx; (void)on; return 0; }
+int fhe_prof_report(fhe_ctx *ctx, char *buf, uint32_t len) { (void)ctx; if (len) buf[0] = 0; return 0; }
+int fhe_launch_count(fhe_ctx *ctx, uint64_t *out) { (void)ctx; *out = 0; return 0; }
+int fhe_peak_modmul(fhe_ctx *ctx, uint32_t iters, double *out) {
+    (void)ctx; (void)iters; *out = 0.0;
+    return fail(FHE_EINVAL, "no device in the golden model");
+}
 int fhe_ctx_key_bytes(fhe_ctx *ctx, uint64_t *out) { *out = ctx->key_bytes; return 0; }
 
 /* ------------------------------------------------------------------ */

@@ -52,6 +52,11 @@ SIGNATURES = {
     "fhe_sync": (c_int, [c_void_p]),
     "fhe_ctx_key_bytes": (c_int, [c_void_p, _U64P]),
     "fhe_keygen_rotations": (c_int, [c_void_p, POINTER(c_uint32), c_uint32]),
+    "fhe_ctx_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "fhe_peak_modmul": (c_int, [c_void_p, c_uint32, POINTER(c_double)]),
+    "fhe_prof_enable": (c_int, [c_void_p, c_int]),
+    "fhe_prof_report": (c_int, [c_void_p, ctypes.c_char_p, c_uint32]),
+    "fhe_launch_count": (c_int, [c_void_p, _U64P]),
     "fhe_ct_create": (c_int, [c_void_p, c_uint32, c_uint32, POINTER(c_void_p)]),
     "fhe_ct_destroy": (None, [c_void_p]),
     "fhe_ct_level": (c_uint32, [c_void_p]),

@@ -27,8 +27,8 @@ struct ModInfo {
     u64 mu;        // floor(2^64 / q)
     u64 ninv, ninv_sh;
     u64 half;      // (q - 1) / 2
-    const u64 *tw, *tw_sh;     // psi^brev(k)  and Shoup companions
-    const u64 *itw, *itw_sh;   // psi^-brev(k) and Shoup companions
+    const ulonglong2 *tw;      // (psi^brev(k), Shoup companion) pairs
+    const ulonglong2 *itw;     // (psi^-brev(k), Shoup companion) pairs
 };
 
 DEV u64 mulhi(u64 a, u64 b) { return __umul64hi(a, b); }

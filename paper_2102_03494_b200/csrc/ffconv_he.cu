@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 #include <unordered_set>
 #include <vector>
@@ -137,11 +138,46 @@ struct fhe_ctx {
     u64 key_bytes = 0;
     // workspaces
     int S = 1;                          // key-switching sub-batch
-    u64 *w_D = nullptr, *w_C0 = nullptr, *w_C1 = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;
+    u64 *w_D = nullptr, *w_C1 = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;
     u64 *w_sq = nullptr;
     size_t w_sq_words = 0;
     u64 *w_tmp = nullptr;
     size_t w_tmp_words = 0;
+    // profiling
+    bool prof = false;
+    u64 launches = 0;
+    struct Rec { const char *name; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> ev_pool;
+};
+
+// bracket one launch with events when profiling is on
+struct ProfScope {
+    fhe_ctx *c;
+    const char *name;
+    cudaEvent_t a = nullptr;
+    ProfScope(fhe_ctx *c_, const char *n) : c(c_), name(n) {
+        c->launches++;
+        if (!c->prof) return;
+        a = take();
+        cudaEventRecord(a, c->st);
+    }
+    cudaEvent_t take() {
+        if (c->ev_pool.empty()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    ~ProfScope() {
+        if (!c->prof) return;
+        cudaEvent_t b = take();
+        cudaEventRecord(b, c->st);
+        c->recs.push_back({name, a, b});
+    }
 };
 
 struct fhe_ct {
@@ -163,14 +199,20 @@ static inline long long nblocks(long long total, int bs = 256) {
     long long b = (total + bs - 1) / bs;
     return b > 148 * 16 ? 148 * 16 : (b < 1 ? 1 : b);
 }
-#define EW(kernel, total, ...) kernel<<<(unsigned)nblocks(total), 256, 0, c->st>>>(__VA_ARGS__)
+#define EW(kernel, total, ...)                                                 \
+    do {                                                                       \
+        ProfScope ps_(c, #kernel);                                             \
+        kernel<<<(unsigned)nblocks(total), 256, 0, c->st>>>(__VA_ARGS__);      \
+    } while (0)
 
 // ----------------------------------------------------- row-kernel dispatch
 static std::mutex g_attr_mu;
 static std::unordered_set<const void *> g_attr_done;
 
 template <int LOGN, typename... KArgs, typename... Args>
-static void launch_row(void (*kern)(KArgs...), dim3 grid, cudaStream_t st, Args... args) {
+static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim3 grid, cudaStream_t st,
+                       Args... args) {
+    ProfScope ps_(c, name);
     using C = NttCfg<LOGN>;
     const size_t smem = (size_t)C::SMEM_WORDS * sizeof(u64);
     {
@@ -201,15 +243,15 @@ static void launch_row(void (*kern)(KArgs...), dim3 grid, cudaStream_t st, Args.
         default: break;                        \
     }
 
-static int ntt_rows(fhe_ctx *c, int rows, const NttRowsArgs &a) {
+static int ntt_rows(fhe_ctx *c, int rows, const NttRowsArgs &a, const char *name = "k_ntt_rows") {
     if (rows <= 0) return 0;
-    LOGN_SWITCH(c->logn, launch_row<LG>(k_ntt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
+    LOGN_SWITCH(c->logn, launch_row<LG>(c, name, k_ntt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
     CHECK_LAUNCH();
     return 0;
 }
-static int intt_rows(fhe_ctx *c, int rows, const InttRowsArgs &a) {
+static int intt_rows(fhe_ctx *c, int rows, const InttRowsArgs &a, const char *name = "k_intt_rows") {
     if (rows <= 0) return 0;
-    LOGN_SWITCH(c->logn, launch_row<LG>(k_intt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
+    LOGN_SWITCH(c->logn, launch_row<LG>(c, name, k_intt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
     CHECK_LAUNCH();
     return 0;
 }
@@ -379,10 +421,10 @@ static int setup_moduli(fhe_ctx *c) {
         u64 *base = tw.data() + (size_t)id * 4 * n;
         for (u32 k = 0; k < n; k++) {
             u64 w = pw[hm::brev(k, c->logn)], wi = pwi[hm::brev(k, c->logn)];
-            base[k] = w;
-            base[n + k] = hm::shoup(w, q);
-            base[2 * n + k] = wi;
-            base[3 * n + k] = hm::shoup(wi, q);
+            base[2 * k] = w;
+            base[2 * k + 1] = hm::shoup(w, q);
+            base[2 * n + 2 * k] = wi;
+            base[2 * n + 2 * k + 1] = hm::shoup(wi, q);
         }
         ModInfo &M = c->hmods[id];
         M.q = q;
@@ -396,7 +438,8 @@ static int setup_moduli(fhe_ctx *c) {
         M.ninv_sh = hm::shoup(M.ninv, q);
         M.half = (q - 1) / 2;
         u64 *dbase = c->d_tw + (size_t)id * 4 * n;
-        M.tw = dbase; M.tw_sh = dbase + n; M.itw = dbase + 2 * n; M.itw_sh = dbase + 3 * n;
+        M.tw = (const ulonglong2 *)dbase;
+        M.itw = (const ulonglong2 *)(dbase + 2 * n);
     }
     CU(cudaMemcpy(c->d_tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice));
     CU(cudaMalloc((void **)&c->d_mods, c->nmod * sizeof(ModInfo)));
@@ -438,15 +481,14 @@ static int setup_secret(fhe_ctx *c) {
 
 static int setup_workspace(fhe_ctx *c) {
     size_t n = c->n, L = c->L;
-    size_t per_ct = n * (3 * L + L * (L + 1) + 2 * (L + 1)) * 8;
-    size_t budget = 96ull << 20;   // keep one sub-batch's intermediates L2-sized
+    size_t per_ct = n * (2 * L + L * (L + 1) + 2 * (L + 1)) * 8;
+    size_t budget = 512ull << 20;
     const char *env = getenv("FHE_KS_BATCH");
     int S = env ? atoi(env) : (int)(budget / per_ct);
     if (S < 1) S = 1;
     if (S > MAXS) S = MAXS;
     c->S = S;
     CU(cudaMalloc((void **)&c->w_D, S * L * n * 8));
-    CU(cudaMalloc((void **)&c->w_C0, S * L * n * 8));
     CU(cudaMalloc((void **)&c->w_C1, S * L * n * 8));
     CU(cudaMalloc((void **)&c->w_Ext, S * L * (L + 1) * n * 8));
     CU(cudaMalloc((void **)&c->w_Acc, S * 2 * (L + 1) * n * 8));
@@ -521,7 +563,7 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto &kv : c->keys) cudaFree(kv.second.d);
     void *bufs[] = {c->d_mods, c->d_tw, c->d_s_can, c->d_s_m, c->d_s2_m, c->d_sk_ids, c->d_slot2ntt,
-                    c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_D, c->w_C0, c->w_C1, c->w_Ext, c->w_Acc, c->w_sq};
+                    c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_D, c->w_C1, c->w_Ext, c->w_Acc, c->w_sq};
     for (void *b : bufs) if (b) cudaFree(b);
     if (c->w_tmp) cudaFreeAsync(c->w_tmp, c->st);
     if (c->st) { cudaStreamSynchronize(c->st); cudaStreamDestroy(c->st); }
@@ -530,6 +572,72 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
 
 extern "C" int fhe_sync(fhe_ctx *c) {
     CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+extern "C" int fhe_ctx_stream(fhe_ctx *c, void **stream) {
+    *stream = (void *)c->st;
+    return 0;
+}
+
+extern "C" int fhe_peak_modmul(fhe_ctx *c, uint32_t iters, double *out) {
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
+    const int blocks = sms * 8, threads = 256;
+    u64 q = c->P.q[0], w = q / 3 + 7, wsh = hm::shoup(w, q);
+    u64 *sink;
+    CU(cudaMallocAsync((void **)&sink, 8, c->st));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    k_peak_modmul<<<blocks, threads, 0, c->st>>>(sink, iters / 8 + 1, q, w, wsh);   // warm-up
+    CU(cudaEventRecord(e0, c->st));
+    k_peak_modmul<<<blocks, threads, 0, c->st>>>(sink, iters, q, w, wsh);
+    CU(cudaEventRecord(e1, c->st));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CU(cudaFreeAsync(sink, c->st));
+    *out = (double)blocks * threads * 8.0 * iters / (ms * 1e-3);
+    return 0;
+}
+
+extern "C" int fhe_prof_enable(fhe_ctx *c, int on) {
+    c->prof = on != 0;
+    return 0;
+}
+
+extern "C" int fhe_prof_report(fhe_ctx *c, char *buf, uint32_t len) {
+    CU(cudaStreamSynchronize(c->st));
+    std::vector<std::pair<std::string, std::pair<long, double>>> agg;
+    for (auto &r : c->recs) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        bool found = false;
+        for (auto &x : agg)
+            if (x.first == r.name) { x.second.first++; x.second.second += ms; found = true; break; }
+        if (!found) agg.push_back({r.name, {1, (double)ms}});
+        c->ev_pool.push_back(r.a);
+        c->ev_pool.push_back(r.b);
+    }
+    c->recs.clear();
+    std::string out;
+    char line[256];
+    for (auto &x : agg) {
+        snprintf(line, sizeof line, "%s %ld %.6f\n", x.first.c_str(), x.second.first, x.second.second);
+        out += line;
+    }
+    if (len) {
+        strncpy(buf, out.c_str(), len - 1);
+        buf[len - 1] = 0;
+    }
+    return 0;
+}
+
+extern "C" int fhe_launch_count(fhe_ctx *c, uint64_t *out) {
+    *out = c->launches;
     return 0;
 }
 
@@ -795,23 +903,27 @@ struct KsOut {
     const u64 *add[MAXS];
     long long out_pstride, add_pstride;
     int add_pmask;
+    u32 add_g;
 };
 
 static int keyswitch_core(fhe_ctx *c, int S, u32 l, const u64 *key, const DigitTab &dt, const KsOut &ko) {
     size_t n = c->n;
     int L = (int)c->L;
     // ModUp: every off-diagonal (digit, prime) pair
-    LOGN_SWITCH(c->logn, launch_row<LG>(k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
+    LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_modup", k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
                                         c->d_mods));
     CHECK_LAUNCH();
-    long long tot = (long long)(l + 1) * n;
-    k_ks_inner<<<(unsigned)nblocks(tot), 256, 0, c->st>>>(c->w_Ext, dt, key, c->w_Acc, S, (int)l, L, (int)c->logn,
-                                                           c->special_id, c->d_mods);
+    long long tot = (long long)((S + 1) / 2) * (l + 1) * n;
+    {
+        ProfScope ps_(c, "k_ks_inner");
+        k_ks_inner<<<(unsigned)nblocks(tot), 256, 0, c->st>>>(c->w_Ext, dt, key, c->w_Acc, S, (int)l, L,
+                                                               (int)c->logn, c->special_id, c->d_mods);
+    }
     CHECK_LAUNCH();
     // ModDown: INTT of the special limb of both accumulators
     InttRowsArgs ia = iargs(c->w_Acc + l * n, c->w_Acc + l * n, (long long)(l + 1) * n);
     ia.map.id[0] = (unsigned char)c->special_id;
-    TRY(intt_rows(c, 2 * S, ia));
+    TRY(intt_rows(c, 2 * S, ia, "k_intt_rows(moddown)"));
     RescaleArgs ra;
     memset(&ra, 0, sizeof ra);
     for (int s = 0; s < S; s++) {
@@ -825,9 +937,10 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const u64 *key, const DigitT
     ra.out_pstride = ko.out_pstride;
     ra.add_pstride = ko.add_pstride;
     ra.add_pmask = ko.add_pmask;
+    ra.add_g = ko.add_g;
     ra.src_id = c->special_id;
     for (u32 i = 0; i < l; i++) { ra.fac[i] = c->pinv[i]; ra.fac_sh[i] = c->pinv_sh[i]; }
-    LOGN_SWITCH(c->logn, launch_row<LG>(k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
+    LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
     CHECK_LAUNCH();
     return 0;
 }
@@ -842,8 +955,8 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
         PtrTab pt;
         memset(&pt, 0, sizeof pt);
         for (int s = 0; s < S; s++) { pt.in[s] = in[b0 + s]; pt.out[s] = out[b0 + s]; }
-        LOGN_SWITCH(c->logn, launch_row<LG>(k_rot_gather_intt<LG>, dim3(S, 2, l), c->st, pt, (int)l, g, c->w_C0,
-                                            c->w_C1, c->w_D, c->d_mods));
+        LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rot_gather_intt", k_rot_gather_intt<LG>, dim3(S, l), c->st, pt,
+                                            (int)l, g, c->w_C1, c->w_D, c->d_mods));
         CHECK_LAUNCH();
         DigitTab dt;
         KsOut ko;
@@ -853,11 +966,12 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
             dt.coef[s] = c->w_D + (size_t)s * l * n;
             dt.ntt[s] = c->w_C1 + (size_t)s * l * n;
             ko.out[s] = out[b0 + s];
-            ko.add[s] = c->w_C0 + (size_t)s * l * n;
+            ko.add[s] = in[b0 + s];          // c0 limbs, read through the automorphism
         }
         ko.out_pstride = (long long)l * n;
         ko.add_pstride = 0;
         ko.add_pmask = 1;
+        ko.add_g = g;
         TRY(keyswitch_core(c, S, l, key, dt, ko));
     }
     return 0;
@@ -915,7 +1029,7 @@ extern "C" int fhe_mod_switch(fhe_ctx *c, const fhe_ct *a, fhe_ct *out) {
     InttRowsArgs ia = iargs(a->d + (l - 1) * n, c->w_tmp, (long long)l * n);
     ia.dA = n;
     ia.map.id[0] = (unsigned char)(l - 1);
-    TRY(intt_rows(c, (int)(cnt * 2), ia));
+    TRY(intt_rows(c, (int)(cnt * 2), ia, "k_intt_rows(modswitch)"));
     const LevelDev &T = c->hlv[l];
     for (size_t b0 = 0; b0 < cnt; b0 += MAXS) {
         int S = (int)std::min<size_t>(MAXS, cnt - b0);
@@ -932,7 +1046,7 @@ extern "C" int fhe_mod_switch(fhe_ctx *c, const fhe_ct *a, fhe_ct *out) {
         ra.out_pstride = (long long)(l - 1) * n;
         ra.src_id = (int)(l - 1);
         for (u32 i = 0; i + 1 < l; i++) { ra.fac[i] = T.msinv[i]; ra.fac_sh[i] = T.msinv_sh[i]; }
-        LOGN_SWITCH(c->logn, launch_row<LG>(k_rescale<LG>, dim3(S, 2, l - 1), c->st, ra, c->d_mods));
+        LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rescale(modswitch)", k_rescale<LG>, dim3(S, 2, l - 1), c->st, ra, c->d_mods));
         CHECK_LAUNCH();
     }
     return 0;

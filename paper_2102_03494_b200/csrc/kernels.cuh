@@ -147,33 +147,25 @@ struct PtrTab {
     u64 *out[MAXS];
 };
 
-// Key switching, step 1 (rotation).  grid (S, 2, l): row (s, p, i) of input
-// ciphertext s.  c0 rows: permuted copy -> C0p[s][i].  c1 rows: permuted copy ->
-// C1p[s][i] (NTT form of digit i, used on the inner-product diagonal), INTT -> D[s][i].
+// Key switching, step 1 (rotation).  grid (S, l): c1 limb i of input ct s.
+// The row is staged in shared memory once; the automorphism is applied as a
+// gather on the way out (C1p[s][i]: NTT-form digit for the inner-product
+// diagonal) and on the first inverse-NTT pass (D[s][i]: coefficient digit).
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt, int l, u32 g, u64 *C0p, u64 *C1p,
-                                                                  u64 *D, const ModInfo *__restrict__ mods) {
+__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt, int l, u32 g, u64 *C1p, u64 *D,
+                                                                  const ModInfo *__restrict__ mods) {
     using C = NttCfg<LOGN>;
     extern __shared__ u64 sm[];
-    const int s = blockIdx.x, p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
+    const int s = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
     const long long n = C::N;
-    const u64 *src = pt.in[s] + ((long long)p * l + i) * n;
+    const u64 *src = pt.in[s] + ((long long)l + i) * n;
     for (int x = tid; x < C::N; x += C::TH) sm[spad(x)] = src[x];
     __syncthreads();
-    u64 w[C::E];
-#pragma unroll
-    for (int e = 0; e < C::E; e++) w[e] = sm[spad(galois_perm(tid + e * C::TH, g, LOGN))];
-    u64 *side = (p == 0 ? C0p : C1p) + ((long long)s * l + i) * n;
-#pragma unroll
-    for (int e = 0; e < C::E; e++) side[tid + e * C::TH] = w[e];
-    if (p == 0) return;
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < C::E; e++) sm[spad(tid + e * C::TH)] = w[e];
-    __syncthreads();
+    u64 *side = C1p + ((long long)s * l + i) * n;
+    for (int x = tid; x < C::N; x += C::TH) side[x] = sm[spad(galois_perm(x, g, LOGN))];
     const ModInfo M = mods[i];
     u64 v[C::E];
-    ntt_inv_core<LOGN>(v, sm, M, tid);
+    ntt_inv_core<LOGN>(v, sm, M, tid, g);
     u64 *dst = D + ((long long)s * l + i) * n;
 #pragma unroll
     for (int e = 0; e < C::E; e++) dst[(e << (LOGN - C::W)) | tid] = v[e];
@@ -216,6 +208,7 @@ struct RescaleArgs {
     const u64 *add[MAXS];         // nullable per s
     long long coef_pstride, base_pstride, out_pstride, add_pstride;
     int add_pmask;                // bit p set: add addend for output poly p
+    u32 add_g;                    // != 0: addend is read through the automorphism X -> X^g
     int src_id;                   // modulus id of the dropped prime
     u64 fac[MAXQ], fac_sh[MAXQ];
 };
@@ -238,11 +231,27 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
     u64 *out = a.out[s] + p * a.out_pstride + i * n;
     const u64 *add = ((a.add_pmask >> p) & 1) && a.add[s] ? a.add[s] + p * a.add_pstride + i * n : nullptr;
     const u64 f = a.fac[i], fsh = a.fac_sh[i];
-    for (int x = tid; x < C::N; x += C::TH) {
-        u64 y = shoup(subm(base[x], sm[spad(x)], M.q) , f, fsh, M.q);
-        if (add) y = addm(y, add[x], M.q);
-        out[x] = y;
+    u64 y[C::E];
+#pragma unroll
+    for (int e = 0; e < C::E; e++) {
+        const int x = tid + e * C::TH;
+        y[e] = shoup(subm(base[x], sm[spad(x)], M.q), f, fsh, M.q);
     }
+    if (add && a.add_g) {
+        __syncthreads();
+        for (int x = tid; x < C::N; x += C::TH) sm[spad(x)] = add[x];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < C::E; e++) {
+            const int x = tid + e * C::TH;
+            y[e] = addm(y[e], sm[spad(galois_perm(x, a.add_g, LOGN))], M.q);
+        }
+    } else if (add) {
+#pragma unroll
+        for (int e = 0; e < C::E; e++) y[e] = addm(y[e], add[tid + e * C::TH], M.q);
+    }
+#pragma unroll
+    for (int e = 0; e < C::E; e++) out[tid + e * C::TH] = y[e];
 }
 
 // ========================================================= elementwise kernels
@@ -251,41 +260,42 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (total); i += (long long)gridDim.x * blockDim.x)
 
 // Key switching, step 3: acc_p[s][i] = sum_j Ext[s][j][i] * key_p[j][i]; keys in
-// Montgomery form, layout [L digits][2][L+1 primes][n].  One thread per (i, x),
-// looping the sub-batch so each key word is loaded once.
+// Montgomery form, layout [L digits][2][L+1 primes][n].  One thread per
+// (pair of cts, prime i, coefficient x): each key word feeds two ciphertexts.
 __global__ void k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, const u64 *__restrict__ key,
                            u64 *__restrict__ Acc, int S, int l, int L, int logn, int special_id,
                            const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
-    GRID_STRIDE(idx, (long long)(l + 1) * n) {
-        const int i = (int)(idx >> logn);
+    const int pairs = (S + 1) / 2;
+    GRID_STRIDE(idx, (long long)pairs * (l + 1) * n) {
         const long long x = idx & (n - 1);
+        const long long r = idx >> logn;
+        const int i = (int)(r % (l + 1));
+        const int s0 = 2 * (int)(r / (l + 1));
+        const bool two = s0 + 1 < S;
         const int kp = i == l ? L : i;
         const ModInfo &M = mods[i == l ? special_id : i];
         const u64 q = M.q, qi = M.qinv;
-        for (int s0 = 0; s0 < S; s0 += 4) {
-            u64 a0[4] = {0, 0, 0, 0}, a1[4] = {0, 0, 0, 0};
-            const int sc = S - s0 < 4 ? S - s0 : 4;
-            for (int j = 0; j < l; j++) {
-                const u64 kb = __ldg(key + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
-                const u64 ka = __ldg(key + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    if (u < sc) {
-                        const u64 e = i == j ? dt.ntt[s0 + u][(long long)j * n + x]
-                                             : Ext[((((long long)(s0 + u) * l + j) * (l + 1)) + i) * n + x];
-                        a0[u] = addm(a0[u], mont(e, kb, q, qi), q);
-                        a1[u] = addm(a1[u], mont(e, ka, q, qi), q);
-                    }
-                }
+        u64 a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+        for (int j = 0; j < l; j++) {
+            const u64 kb = __ldg(key + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
+            const u64 ka = __ldg(key + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
+            const u64 e0 = i == j ? dt.ntt[s0][(long long)j * n + x]
+                                  : Ext[((((long long)s0 * l + j) * (l + 1)) + i) * n + x];
+            a00 = addm(a00, mont(e0, kb, q, qi), q);
+            a01 = addm(a01, mont(e0, ka, q, qi), q);
+            if (two) {
+                const u64 e1 = i == j ? dt.ntt[s0 + 1][(long long)j * n + x]
+                                      : Ext[((((long long)(s0 + 1) * l + j) * (l + 1)) + i) * n + x];
+                a10 = addm(a10, mont(e1, kb, q, qi), q);
+                a11 = addm(a11, mont(e1, ka, q, qi), q);
             }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                if (u < sc) {
-                    Acc[(((long long)(s0 + u) * 2 + 0) * (l + 1) + i) * n + x] = a0[u];
-                    Acc[(((long long)(s0 + u) * 2 + 1) * (l + 1) + i) * n + x] = a1[u];
-                }
-            }
+        }
+        Acc[(((long long)s0 * 2 + 0) * (l + 1) + i) * n + x] = a00;
+        Acc[(((long long)s0 * 2 + 1) * (l + 1) + i) * n + x] = a01;
+        if (two) {
+            Acc[(((long long)(s0 + 1) * 2 + 0) * (l + 1) + i) * n + x] = a10;
+            Acc[(((long long)(s0 + 1) * 2 + 1) * (l + 1) + i) * n + x] = a11;
         }
     }
 }
@@ -611,4 +621,20 @@ __global__ void k_from_mont(const u64 *__restrict__ in, u64 *__restrict__ out, l
         const ModInfo &M = mods[(int)((idx >> logn) % L)];
         out[idx] = mont(in[idx], 1, M.q, M.qinv);
     }
+}
+
+// integer-pipe roofline probe: 8 independent chains of lazy Shoup modmuls per
+// thread, register resident; counts 8 * iters modmuls per thread.
+__global__ void k_peak_modmul(u64 *sink, u32 iters, u64 q, u64 w, u64 wsh) {
+    u64 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) x[k] = threadIdx.x * 8 + k + blockIdx.x;
+    for (u32 it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) x[k] = shoup_lazy(x[k], w, wsh, q);
+    }
+    u64 acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) acc ^= x[k];
+    if (acc == 0x1234567ull) sink[0] = acc;
 }

@@ -59,7 +59,8 @@ DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int 
                 if (e & (1 << b)) continue;
                 const int e2 = e | (1 << b);
                 const u32 g = (1u << s) + ((u32)fidx<W>(tid, e, f0) >> (LOGN - s));
-                const u64 w = __ldg(M.tw + g), wsh = __ldg(M.tw_sh + g);
+                const ulonglong2 tw = __ldg(M.tw + g);
+                const u64 w = tw.x, wsh = tw.y;
                 u64 U = v[e];
                 U = U >= q2 ? U - q2 : U;
                 u64 V = shoup_lazy(v[e2], w, wsh, q);
@@ -85,7 +86,7 @@ DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int 
 // Out: v[e] = a[(e << (LOGN-W)) | tid] canonical, scaled by n^-1.  Shared memory is
 // free for reuse only after a __syncthreads() by the caller.
 template <int LOGN>
-DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int tid) {
+DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int tid, u32 g_perm = 0) {
     using C = NttCfg<LOGN>;
     constexpr int W = C::W, E = C::E, NP = C::NP, N = C::N;
     const u64 q = M.q, q2 = 2 * q;
@@ -94,8 +95,13 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int 
         const int lt0 = p * W;                                   // log2 t of the first stage
         const int f0 = (lt0 + W) <= LOGN ? lt0 : LOGN - W;
         const int k = (LOGN - lt0) < W ? (LOGN - lt0) : W;
+        if (p == 0 && g_perm) {
 #pragma unroll
-        for (int e = 0; e < E; e++) v[e] = sm[spad(fidx<W>(tid, e, f0))];
+            for (int e = 0; e < E; e++) v[e] = sm[spad(galois_perm(fidx<W>(tid, e, f0), g_perm, LOGN))];
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; e++) v[e] = sm[spad(fidx<W>(tid, e, f0))];
+        }
         if (p < NP - 1) __syncthreads();
 #pragma unroll
         for (int ls = 0; ls < k; ls++) {
@@ -107,7 +113,8 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int 
                 if (e & (1 << b)) continue;
                 const int e2 = e | (1 << b);
                 const u32 g = (u32)h + ((u32)fidx<W>(tid, e, f0) >> (lt + 1));
-                const u64 w = __ldg(M.itw + g), wsh = __ldg(M.itw_sh + g);
+                const ulonglong2 tw = __ldg(M.itw + g);
+                const u64 w = tw.x, wsh = tw.y;
                 u64 U = v[e], V = v[e2];
                 u64 s = U + V;
                 v[e] = s >= q2 ? s - q2 : s;

@@ -128,10 +128,13 @@ class Evaluator:
         self.lib.call("fhe_encrypt", self.ctx, u64_ptr(s), nonce & 0xFFFFFFFF, ct.ptr)
         return ct
 
-    def decrypt(self, ct: Ciphertext) -> np.ndarray:
-        out = np.empty((self.T, ct.rows, self.n), dtype=np.uint64)
+    def decrypt(self, ct: Ciphertext, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.T, ct.rows, self.n), dtype=np.uint64)
+        elif out.dtype != np.uint64 or out.size != self.T * ct.rows * self.n or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError("decrypt: out must be a contiguous uint64 array of T*R*n words")
         self.lib.call("fhe_decrypt", self.ctx, ct.ptr, u64_ptr(out))
-        return out
+        return out.reshape(self.T, ct.rows, self.n)
 
     def decrypt_raw(self, ct: Ciphertext) -> np.ndarray:
         out = np.empty((self.T * ct.rows, ct.level, self.n), dtype=np.uint64)
