@@ -227,6 +227,16 @@ class HeContext:
             self._ev = Evaluator(rp, self._lib)
         return self._ev
 
+    @property
+    def group_size(self) -> int:
+        """Independent outputs a layer keeps in flight: ~1/4 of a device-memory
+        budget (FHE_GROUP_BUDGET_GB, default 24) over the bytes of one handle."""
+        import os
+        ev = self.evaluator
+        handle = ev.T * self.rows * 2 * ev.L * ev.n * 8
+        budget = float(os.environ.get("FHE_GROUP_BUDGET_GB", "24")) * (1 << 30)
+        return max(1, int(budget / (4 * handle)))
+
     def _wrap(self, handle, depth, assembly_depth=0) -> SlotCiphertext:
         return SlotCiphertext(handle, depth, self.params, assembly_depth, ctx=self)
 

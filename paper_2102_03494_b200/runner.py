@@ -1,0 +1,323 @@
+"""Plan execution on the GPU evaluator.
+
+Mirror of `cipherpack.runner.run_encrypted` (/root/reference/pkg/src/cipherpack/runner.py:290-433):
+the same plan walk (step ops -> packing/engine calls), per-step measured
+counters, depth bookkeeping and logits extraction, for a batch of images per
+context.  Differences:
+
+* the context is the sm_100a RNS-BFV evaluator; its parameters are chosen here
+  (`inference_params`): plaintext CRT primes sized from the static worst-case
+  logit bound (runner.py:233-266) and a q chain sized by a per-op noise model;
+* the plaintext reference computation and the run ledger (runner.py:301-313)
+  are not part of this path -- parity is checked by tests against the oracle;
+* FC outputs that are later combined are masked to slot 0 (`mask_fc`, the F4
+  fix); with mask_fc=False the reference's own (diverging)
+  encrypted result is reproduced.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .engine import (
+    BiasVector,
+    WeightMatrix,
+    avg_pool_weights,
+    conv_conv,
+    conv_dense,
+    conv_dense_to_channels,
+    factored_conv,
+    fc_dense,
+    packed_depth,
+    square_layer,
+)
+from .hesim import HeContext, OpCounters, SchemeParams
+from .netspec import NetworkSpec, WeightSet, validate_weights
+from .packing import (
+    ChannelPacked,
+    DensePacked,
+    KernelSpec,
+    channel_unpack,
+    channels_to_dense,
+    conv_pack,
+    dense_pack,
+    dense_unpack,
+    h_grouping,
+    h_grouping_from_dense,
+    h_im2col_from_conv,
+    h_im2col_from_dense,
+    plain_im2col,
+)
+from .params import RlweParams, ntt_primes
+from .planner import (
+    COMBINE, CONV_COLUMNS, CONV_DENSE, FC, FFCONV, GROUP_CONV, GROUP_DENSE, HIM2COL_CONV, HIM2COL_DENSE,
+    PACK_COLUMNS, PACK_DENSE, SQUARE, PackingPlan,
+)
+
+
+def weights_to_matrix(w4d: np.ndarray) -> np.ndarray:
+    """(d, d, in_c, out_c) filters -> K x O_c, rows channel-major (ch, ky, kx) (factorize.py:47-58)."""
+    d1, d2, ic, oc = w4d.shape
+    if d1 != d2:
+        raise ValueError(f"kernel must be square, got {d1}x{d2}")
+    return w4d.transpose(2, 0, 1, 3).reshape(d1 * d2 * ic, oc)
+
+
+def _conv_w(ws, i):
+    t = ws[f"layer{i}.weight"]
+    return WeightMatrix(weights_to_matrix(t.values), t.bits, t.scale)
+
+
+def _ff_w(ws, i):
+    a, b = ws[f"layer{i}.w1"], ws[f"layer{i}.w2"]
+    return (WeightMatrix(weights_to_matrix(a.values), a.bits, a.scale),
+            WeightMatrix(weights_to_matrix(b.values), b.bits, b.scale))
+
+
+def _fc_w(ws, i):
+    t, b = ws[f"layer{i}.weight"], ws[f"layer{i}.bias"]
+    return WeightMatrix(t.values, t.bits, t.scale), BiasVector(b.values, b.scale)
+
+
+# ----------------------------------------------------------- static bounds
+
+def _max_col_l1(m) -> int:
+    return int(np.max(np.sum(np.abs(np.asarray(m).astype(object)), axis=0))) if np.size(m) else 0
+
+
+def static_bounds(net: NetworkSpec, ws: WeightSet, input_bound: int) -> list[int]:
+    """Worst-case |value| after every layer for inputs in [-input_bound, input_bound]
+    (runner.py:233-266)."""
+    b = int(input_bound)
+    out = []
+    for i, layer in enumerate(net.layers):
+        if layer.kind == "conv":
+            b *= _max_col_l1(weights_to_matrix(ws[f"layer{i}.weight"].values))
+        elif layer.kind == "ffconv":
+            b *= _max_col_l1(weights_to_matrix(ws[f"layer{i}.w1"].values))
+            b *= _max_col_l1(weights_to_matrix(ws[f"layer{i}.w2"].values))
+        elif layer.kind == "square":
+            b *= b
+        elif layer.kind == "avgpool":
+            b *= layer.d * layer.d
+        elif layer.kind == "fc":
+            bias = ws[f"layer{i}.bias"].values
+            b = b * _max_col_l1(ws[f"layer{i}.weight"].values) + (int(np.max(np.abs(bias))) if bias.size else 0)
+        out.append(b)
+    return out
+
+
+# ----------------------------------------------------------- parameters
+
+# per-op invariant-noise cost in bits (t_bits = log2 of the plaintext prime);
+# calibrated with scripts/noise_probe.py on the B200
+def _noise_bits(plan: PackingPlan, t_bits: float, mask_fc: bool) -> float:
+    need = t_bits + 10.0                              # fresh encryption
+    for k, step in enumerate(plan.steps):
+        op = step.op
+        if op in (CONV_DENSE,) or (op == FFCONV and step.pattern in ("DP-HI2C-CP", "DP-DP")):
+            need += t_bits + 14 + t_bits + 3 + 8          # dot product + slot mask + assembly chain
+        if op == FFCONV:
+            need += 10                                    # 1x1 (scalar) stage(s)
+            if step.pattern in ("CP-HI2C-CP", "CP-HI2C-DP"):
+                need += 10
+            if step.pattern == "DP-DP":
+                need += t_bits + 14 + t_bits + 3 + 8
+        if op == CONV_COLUMNS:
+            need += 12
+        if op in (HIM2COL_DENSE, HIM2COL_CONV, GROUP_DENSE):
+            need += t_bits + 3 + 12
+        if op == SQUARE:
+            need += t_bits + 12
+        if op == FC:
+            need += t_bits + 14
+            nxt = plan.steps[k + 1].op if k + 1 < len(plan.steps) else None
+            if mask_fc and nxt == COMBINE:
+                need += t_bits + 3
+        if op == COMBINE:
+            need += 8
+    return need + 20.0                                # safety margin
+
+
+def inference_params(net: NetworkSpec, plan: PackingPlan, ws: WeightSet, input_bound: int, *,
+                     t_bits: int = 30, q_bits: int = 60, mask_fc: bool = True, seed: int | None = None) -> RlweParams:
+    """Plaintext CRT primes covering 2 * static bound, and a q chain for the plan."""
+    n_slots = net.scheme.n_slots
+    two_n = 4 * n_slots
+    bound = max(static_bounds(net, ws, input_bound) + [input_bound, 1])
+    cands = ntt_primes(t_bits, 64, two_n)
+    ts, total = [], 1
+    for p in cands:
+        ts.append(p)
+        total *= p
+        if total > 2 * bound:
+            break
+    need = _noise_bits(plan, math.log2(ts[0]), mask_fc)
+    L = max(2, math.ceil(need / q_bits))
+    q = ntt_primes(q_bits, L, two_n, exclude=ts)
+    p = ntt_primes(min(q_bits + 1, 61), 1, two_n, exclude=ts + q)
+    b = ntt_primes(60, L + 1, two_n, exclude=ts + q + p)
+    if sum(math.log2(x) for x in b) < sum(math.log2(x) for x in q) + math.log2(2 * n_slots) + t_bits + 4:
+        b = ntt_primes(60, L + 2, two_n, exclude=ts + q + p)
+    kw = {} if seed is None else {"seed": seed}
+    return RlweParams(log_n=n_slots.bit_length(), q=tuple(q), p=tuple(p), t=tuple(ts), b=tuple(b), **kw)
+
+
+def scheme_for(params: RlweParams, rotation_weight: float = 10.0) -> SchemeParams:
+    """A SchemeParams whose t is the CRT product of the chosen plaintext primes."""
+    return SchemeParams(n_slots=params.n_slots, t=params.t_product, rotation_weight=rotation_weight,
+                        t_factors=params.t, rlwe=params)
+
+
+# ----------------------------------------------------------- execution
+
+@dataclass
+class StepRecord:
+    label: str
+    op: str
+    pattern: str | None
+    phases: list          # [(name, OpCounters)]
+
+
+@dataclass
+class RunResult:
+    logits: np.ndarray | None          # (B, n_out) object ints, or (n_out,) for batch 1
+    steps: list
+    counters: OpCounters
+    depth: int
+    assembly_depth: int
+    layer_depths: list = field(default_factory=list)
+    layer_outputs: list = field(default_factory=list)
+    elided_rotations: int = 0
+
+
+def _logits(value, ctx):
+    batch = getattr(ctx, "batch", 1)
+
+    def dec(ct, k):
+        v = np.asarray(ctx.decrypt(ct), dtype=object)
+        v = v[None] if v.ndim == 1 else v
+        return v[:, :k]
+
+    if isinstance(value, DensePacked):
+        out = dec(value.ct, value.occupied)
+    elif isinstance(value, ChannelPacked):
+        out = np.concatenate([dec(c, value.rows) for c in value.cts], axis=1)
+    else:
+        raise ValueError(f"cannot extract logits from {type(value)!r}")
+    return out[0] if batch == 1 else out
+
+
+def _tensor(value, ctx):
+    if isinstance(value, DensePacked):
+        return dense_unpack(value, ctx)
+    if isinstance(value, ChannelPacked):
+        return channel_unpack(value, ctx)
+    return None
+
+
+def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input_tensor, *,
+                  ctx=None, track_values: bool = True, capture_layers: bool = False,
+                  mask_fc: bool = True) -> RunResult:
+    """Walk the plan over an evaluation context (runner.py:290-409).
+
+    input_tensor: (c, h, w) for a batch-1 context or (B, c, h, w).
+    ctx: any object with the HeContext interface; default: a GPU HeContext on
+    net.scheme (its parameters must then be batching-compatible)."""
+    validate_weights(net, weights)
+    if plan.net != net:
+        raise ValueError("plan was built for a different network")
+    if ctx is None:
+        ctx = HeContext(net.scheme)
+    x_in = None
+    if track_values:
+        x_in = np.asarray(input_tensor)
+        shape = (net.input_shape.c, net.input_shape.h, net.input_shape.w)
+        if x_in.shape[-3:] != shape:
+            raise ValueError(f"input shape {x_in.shape} does not match (c, h, w) = {shape}")
+    records, layer_depths, layer_outputs = [], [], []
+    value = None
+    for k, step in enumerate(plan.steps):
+        before = ctx.counters.copy()
+        d_before = packed_depth(value) if value is not None else (0, 0)
+        phases = None
+        op = step.op
+        if op == PACK_DENSE:
+            value = dense_pack(x_in if track_values else np.zeros((step.in_shape.c, step.in_shape.h,
+                                                                   step.in_shape.w), dtype=np.int64),
+                               ctx, tracked=track_values)
+        elif op == PACK_COLUMNS:
+            ow, oh = step.kernel.out_dims(step.in_shape)
+            cols = (plain_im2col(x_in, step.kernel) if track_values else
+                    np.zeros((ow * oh, step.kernel.k_columns(step.in_shape.c)), dtype=np.int64))
+            value = conv_pack(cols, ctx, (ow, oh), tracked=track_values)
+        elif op == COMBINE:
+            value = channels_to_dense(value, ctx)
+        elif op == HIM2COL_DENSE:
+            value = h_im2col_from_dense(value, step.kernel, ctx)
+        elif op == HIM2COL_CONV:
+            value = h_im2col_from_conv(value, step.kernel, ctx)
+        elif op == GROUP_DENSE:
+            value = h_grouping_from_dense(value, KernelSpec(1, 1), ctx)
+        elif op == GROUP_CONV:
+            value = h_grouping(value, KernelSpec(1, 1))
+        elif op == SQUARE:
+            value, phases = square_layer(value, ctx)
+        elif op in (CONV_DENSE, CONV_COLUMNS):
+            i = step.layer_index
+            w = avg_pool_weights(step.kernel, step.in_shape.c) if step.pooling else _conv_w(weights, i)
+            value, phases = (conv_dense(value, w, step.kernel, ctx) if op == CONV_DENSE
+                             else conv_conv(value, w, ctx))
+        elif op == FC:
+            w, bias = _fc_w(weights, step.layer_index)
+            nxt = plan.steps[k + 1].op if k + 1 < len(plan.steps) else None
+            outs, phases = fc_dense(value, w, bias, ctx, mask_outputs=mask_fc and nxt == COMBINE)
+            value = ChannelPacked(tuple(outs), (1, 1))
+        elif op == FFCONV:
+            value, phases = _run_ffconv(step, value, weights, ctx)
+        else:
+            raise ValueError(f"cannot execute step {op!r}")
+        if phases is None:
+            phases = [("total", ctx.counters - before)]
+        else:
+            phases = [(p.name, p.counters) for p in phases]
+        records.append(StepRecord(step.label(), op, step.pattern, phases))
+        if step.layer_index is not None and op in (SQUARE, CONV_DENSE, CONV_COLUMNS, FC, FFCONV):
+            d_after = packed_depth(value)
+            layer_depths.append({"layer_index": step.layer_index, "op": op, "pattern": step.pattern,
+                                 "depth_delta": d_after[0] - d_before[0],
+                                 "assembly_delta": d_after[1] - d_before[1]})
+            if capture_layers and track_values:
+                layer_outputs.append((step.layer_index, _tensor(value, ctx)))
+    logits = _logits(value, ctx) if track_values else None
+    depth, adepth = packed_depth(value)
+    return RunResult(logits, records, ctx.counters.copy(), depth, adepth, layer_depths, layer_outputs,
+                     ctx.elided_rotations)
+
+
+def _run_ffconv(step, value, ws, ctx):
+    w1, w2 = _ff_w(ws, step.layer_index)
+    pat = step.pattern
+    if pat in ("DP-HI2C-CP", "CP-HI2C-CP"):
+        return factored_conv(value, w1, w2, step.kernel, pat, ctx)
+    rank_k = KernelSpec(step.kernel.d, step.kernel.stride, step.rank)
+    one = KernelSpec(1, 1, step.kernel.out_channels)
+    if pat == "DP-DP":
+        mid, p1 = conv_dense(value, w1, rank_k, ctx)
+        out, p2 = conv_dense(mid, w2, one, ctx)
+        names = ["w1-dots", "w1-assembly", "w2-dots", "w2-assembly"]
+        return out, [type(p)(n, p.counters) for p, n in zip(p1 + p2, names)]
+    if pat == "CP-HI2C-DP":
+        mid, p1 = conv_conv(value, w1, ctx)
+        before = ctx.counters.copy()
+        dense_mid = channels_to_dense(mid, ctx)
+        comb = ctx.counters - before
+        out, p2 = conv_dense(dense_mid, w2, one, ctx)
+        from .engine import PhaseCost
+        phases = [PhaseCost("w1", p1[0].counters), PhaseCost("mid-combine", comb),
+                  PhaseCost("w2-dots", p2[0].counters), PhaseCost("w2-assembly", p2[1].counters)]
+        return out, phases
+    raise ValueError(f"unknown factorized pattern {pat!r}")

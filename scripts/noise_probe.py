@@ -63,7 +63,7 @@ def probe(t_bits, q_bits, L, combine_len=(168, 100), modswitch=False):
     rec("w1 mask", y)
     y = chain(y, combine_len[0])
     rec("w1 combine", y)
-    y = ev.add(ev.mul_scalar(y, 127), ev.mul_scalar(y, -127))
+    y = ev.add(ev.mul_scalar(y, 127), ev.mul_scalar(ev.rotate(y, 1), -113))
     rec("w2 scalar", y)
     y = chain(y, 4)
     rec("combine5", y)
@@ -84,7 +84,7 @@ def probe(t_bits, q_bits, L, combine_len=(168, 100), modswitch=False):
 
 
 if __name__ == "__main__":
-    settings = [(20, 58, 6), (25, 58, 6), (25, 58, 7), (30, 58, 7), (30, 60, 7), (36, 60, 7)]
+    settings = [(20, 58, 5), (20, 58, 6), (25, 58, 6), (25, 60, 6), (30, 60, 6), (30, 60, 7)]
     if len(sys.argv) > 1:
         settings = [tuple(int(v) for v in s.split(",")) for s in sys.argv[1:]]
     for tb, qb, L in settings:
