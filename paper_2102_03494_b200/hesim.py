@@ -232,7 +232,9 @@ class HeContext:
         """Independent outputs a layer keeps in flight: ~1/4 of a device-memory
         budget (FHE_GROUP_BUDGET_GB, default 24) over the bytes of one handle."""
         import os
-        ev = self.evaluator
+        if self._ev is None:          # count-only walk: no device memory involved
+            return 1 << 30
+        ev = self._ev
         handle = ev.T * self.rows * 2 * ev.L * ev.n * 8
         budget = float(os.environ.get("FHE_GROUP_BUDGET_GB", "24")) * (1 << 30)
         return max(1, int(budget / (4 * handle)))

@@ -1,0 +1,68 @@
+"""The reference-facing API on the sm_100a CUDA library (B200 only).
+
+* every reference primitive sequence (hesim_sequences.json) decrypts, counts and
+  tracks depth as the reference did;
+* random FFConv-shaped networks (networks.json): logits, per-step op counts,
+  depths and per-layer tensors equal the reference's, and the output
+  ciphertexts equal the golden model's word for word;
+* BASELINE configs[0] end to end: logits equal run_reference (fixture) for two
+  synthetic images in one ciphertext row pair, under 5-prime plaintext CRT.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2102_03494_b200.hesim import HeContext
+from paper_2102_03494_b200.planner import build_plan
+from paper_2102_03494_b200.runner import inference_params, run_encrypted, scheme_for
+
+from _shared import cfg0_network, load, network_from_fixture, reference_step_totals, replay, scheme_from, step_totals
+
+pytestmark = pytest.mark.gpu
+
+
+def test_reference_sequences_on_gpu(cuda_lib):
+    for case in load("hesim_sequences.json"):
+        ctx = HeContext(scheme_from(case["n_slots"], case["t_factors"], levels=8), lib=cuda_lib, debug_checks=True)
+        ct = replay(ctx, case)
+        assert [int(v) for v in ctx.decrypt(ct)] == case["expect"]
+        c = ctx.counters
+        assert [c.mul_pc, c.add_cc, c.rot, c.mul_cc, c.assembly_mul_pc] == case["counters"]
+        assert (ct.depth, ct.assembly_depth) == (case["depth"], case["assembly_depth"])
+
+
+def test_networks_on_gpu_match_reference_and_golden(cuda_lib, golden_lib):
+    for k, fx in enumerate(load("networks.json")):
+        net, ws = network_from_fixture(fx)
+        plan = build_plan(net, "explicit")
+        x = np.array(fx["inputs"])
+        gpu = HeContext(net.scheme, batch=2, lib=cuda_lib)
+        res = run_encrypted(net, plan, ws, x, ctx=gpu, capture_layers=True)
+        assert [[int(v) for v in row] for row in res.logits] == fx["logits"]
+        assert step_totals(res.steps) == reference_step_totals(fx["rows"])
+        assert (res.depth, res.assembly_depth) == (fx["depth"], fx["assembly_depth"])
+        for (idx, got), r0, r1 in zip(res.layer_outputs, fx["layer_outputs"][0], fx["layer_outputs"][1]):
+            assert np.asarray(got[0]).astype(str).tolist() == r0
+            assert np.asarray(got[1]).astype(str).tolist() == r1
+        if k < 4:
+            gold = HeContext(net.scheme, batch=2, lib=golden_lib)
+            res_g = run_encrypted(net, plan, ws, x, ctx=gold)
+            for a, b in zip(res.value.cts, res_g.value.cts):
+                assert np.array_equal(gpu.evaluator.read(a.handle), gold.evaluator.read(b.handle))
+
+
+def test_cfg0_end_to_end_on_gpu(cuda_lib):
+    from paper_2102_03494_b200.hesim import SchemeParams
+    net0, ws, xs, meta = cfg0_network(SchemeParams(n_slots=8192, t=(1 << 61) - 1))
+    plan0 = build_plan(net0, "explicit")
+    rp = inference_params(net0, plan0, ws, input_bound=255)
+    assert len(rp.t) == 5 and rp.L == 6 and rp.log_qp <= 438
+    net, _, _, _ = cfg0_network(scheme_for(rp))
+    plan = build_plan(net, "explicit")
+    ctx = HeContext(net.scheme, batch=2, lib=cuda_lib)
+    res = run_encrypted(net, plan, ws, xs, ctx=ctx)
+    for row, want in zip(res.logits, meta["logits"]):
+        assert [str(int(v)) for v in row] == want
+    c = res.counters
+    assert (c.mul_pc, c.add_cc, c.rot, c.mul_cc, c.assembly_mul_pc) == (458, 4894, 4889, 2, 438)
+    assert min(ctx.noise_budget(ct) for ct in res.value.cts) > 5
