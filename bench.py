@@ -333,6 +333,139 @@ def run_rotation(args, rank, world, local_rank):
     return result
 
 
+# ------------------------------------------------------------ inference arm
+def cfg0_setup(images: int, seed: int, offset: int = 0):
+    """BASELINE configs[0]/[2] network on seeded synthetic MNIST-shaped images:
+    28x28 pixels round(U[0,1]*255), zero-padded to 29x29 (valid convs, SURVEY.md F5);
+    weights N(0, 0.1) -> 8-bit symmetric quantization; zero biases."""
+    from paper_2102_03494_b200.hesim import SchemeParams
+    from paper_2102_03494_b200.netspec import LayerSpec, NetworkSpec, synthetic_weights
+    from paper_2102_03494_b200.packing import TensorShape
+    from paper_2102_03494_b200.planner import build_plan
+    from paper_2102_03494_b200.runner import inference_params, scheme_for
+
+    layers = (LayerSpec("ffconv", d=5, stride=2, out_channels=5, rank=2, packing_hint="dp-hi2c-cp"),
+              LayerSpec("square"), LayerSpec("fc", out_channels=100), LayerSpec("square"),
+              LayerSpec("fc", out_channels=10))
+    shape = TensorShape(29, 29, 1)
+    prov = NetworkSpec(SchemeParams(n_slots=8192, t=(1 << 61) - 1), shape, layers)
+    ws = synthetic_weights(prov, np.random.default_rng(seed), sigma=0.1)
+    rp = inference_params(prov, build_plan(prov, "explicit"), ws, input_bound=255)
+    net = NetworkSpec(scheme_for(rp), shape, layers)
+    plan = build_plan(net, "explicit")
+    rng = np.random.default_rng(seed + 1)
+    pix = np.round(rng.random(size=(offset + images, 1, 28, 28)) * 255).astype(np.int64)[offset:]
+    xs = np.zeros((images, 1, 29, 29), dtype=np.int64)
+    xs[:, :, :28, :28] = pix
+    return net, plan, ws, xs, rp
+
+
+def rotation_modmuls_L(n, l):
+    return rotation_modmuls(n, l)
+
+
+def run_inference(args, rank, world, local_rank, images_total=None, steps=None, warmup=None):
+    import torch
+    from paper_2102_03494_b200.abi import cuda_library
+    from paper_2102_03494_b200.hesim import HeContext
+    from paper_2102_03494_b200.runner import pack_input, run_encrypted
+
+    torch.cuda.set_device(local_rank)
+    lib = cuda_library()
+    images_total = images_total or args.images
+    steps = steps if steps is not None else args.steps
+    warmup = warmup if warmup is not None else args.warmup
+    per_rank = images_total // world
+    chunk = min(args.chunk, per_rank)
+    net, plan, ws, xs, rp = cfg0_setup(per_rank, seed=CFG1["seed"], offset=rank * per_rank)
+    ctx = HeContext(net.scheme, batch=chunk, lib=lib)
+    ev = ctx.evaluator
+    stream_ptr = ctypes.c_void_p()
+    lib.call("fhe_ctx_stream", ev.ctx, ctypes.byref(stream_ptr))
+    stream = torch.cuda.ExternalStream(stream_ptr.value, device=local_rank)
+    chunks = [xs[i:i + chunk] for i in range(0, per_rank, chunk)]
+
+    def evaluate(packed_list):
+        return [run_encrypted(net, plan, ws, None, ctx=ctx, packed=p, decrypt=False) for p in packed_list]
+
+    packed = [pack_input(net, plan, c, ctx) for c in chunks]
+    for _ in range(max(1, warmup)):
+        evaluate(packed[:1])
+    ev.sync()
+    if world > 1:
+        torch.distributed.barrier()
+    cnt0 = ctypes.c_uint64()
+    lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt0))
+    rot0 = ctx.counters.rot
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            evaluate(packed)
+        e1.record(stream)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    cnt1 = ctypes.c_uint64()
+    lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt1))
+    rots = ctx.counters.rot - rot0
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{local_rank}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    # e2e: host images -> encrypt -> evaluate -> decrypt logits to host
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    logits = [run_encrypted(net, plan, ws, c, ctx=ctx).logits for c in chunks]
+    ev.sync()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local_rank}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    # physical ciphertext rotations: logical rotations x CRT primes x row pairs
+    phys_rot = rots * rp.T * ctx.rows
+    mm = phys_rot * rotation_modmuls(rp.n, rp.L)
+    return {
+        "images_per_s": images_total * steps / (ms * 1e-3),
+        "ms_per_step": ms / steps,
+        "e2e_images_per_s": images_total / e2e_s,
+        "per_rank_images": per_rank, "chunk": chunk, "chunks": len(chunks),
+        "crt_primes": len(rp.t), "t_bits": round(math.log2(rp.t[0]), 2), "L": rp.L,
+        "log_qp": round(rp.log_qp, 1), "logical_rotations_per_chunk": rots // max(1, steps * len(chunks)),
+        "physical_rotations_per_s": world * phys_rot / (ms * 1e-3),
+        "rotation_modmul_per_s_per_gpu": mm / (ms * 1e-3),
+        "gpu_launches": int(cnt1.value - cnt0.value),
+        "h2d_bytes_per_step": int(xs.size * 8 * world), "d2h_bytes_per_step": int(10 * images_total * 8 * rp.T),
+        "clocks": clk.summary(), "logits_sample": [str(int(v)) for v in np.asarray(logits[0])[0][:3]],
+    }
+
+
+def cpu_baseline_inference(images: int = 1):
+    """Reference algorithm on the host: the product's plan walk over the slot
+    oracle (np.int64 slot engine), one run per plaintext CRT prime, 1 core."""
+    from oracle.slot_oracle import Params, SlotContext
+    from paper_2102_03494_b200.runner import run_encrypted
+    net, plan, ws, xs, rp = cfg0_setup(images, seed=CFG1["seed"])
+    t0 = time.perf_counter()
+    for x in xs:
+        for ti in rp.t:
+            ctx = SlotContext(Params(8192, ti))
+            run_encrypted(net, plan, ws, x, ctx=ctx)
+    el = time.perf_counter() - t0
+    return images / el, f"{images} image(s) x {len(rp.t)} CRT primes, cfg0 plan on the slot oracle"
+
+
+def _cpu_inference_task(args):
+    img_idx, ti = args
+    from oracle.slot_oracle import Params, SlotContext
+    from paper_2102_03494_b200.runner import run_encrypted
+    net, plan, ws, xs, rp = cfg0_setup(1, seed=CFG1["seed"], offset=img_idx)
+    run_encrypted(net, plan, ws, xs[0], ctx=SlotContext(Params(8192, ti)))
+    return 1
+
+
 def _hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -345,6 +478,31 @@ def run_reference_arm(args, rank, world):
     if rank != 0:
         return None
     cores = os.cpu_count() or 1
+    if args.workload == "inference":
+        import multiprocessing as mp
+        _, _, _, _, rp = cfg0_setup(1, seed=CFG1["seed"])
+        sample = max(cores, 8)
+        tasks = [(i, ti) for i in range(sample) for ti in rp.t]
+        rates = []
+        with mp.Pool(cores) as pool:
+            for it in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                pool.map(_cpu_inference_task, tasks)
+                el = time.perf_counter() - t0
+                if it >= args.warmup:
+                    rates.append(sample / el)
+        v = statistics.median(rates)
+        return {
+            "impl": "reference", "metric": "encrypted-image inferences/s (FFConv MNIST-shaped HECNN, cfg2)",
+            "value": v, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sample / v, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": "configs[2] (reference slot-engine algorithm, one run per CRT prime)"},
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "kind": "port",
+                             "sample": f"{sample} images x {len(rp.t)} CRT primes per step"},
+            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "the reference is a slot simulator with no cryptography",
+        }
     rates = []
     for _ in range(args.warmup):
         cpu_baseline_rotation(cores, seconds=0.5)
@@ -371,7 +529,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["rotation"], default="rotation")
+    ap.add_argument("--workload", choices=["rotation", "inference"], default="rotation")
+    ap.add_argument("--images", type=int, default=256, help="inference: images per step (whole job)")
+    ap.add_argument("--chunk", type=int, default=64, help="inference: images per ciphertext batch")
+    ap.add_argument("--no-inference", action="store_true", help="rotation workload: skip the inference sample")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -385,12 +546,40 @@ def main():
         import torch
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    if args.workload == "inference":
+        inf = run_inference(args, rank, world, local_rank)
+        res = {
+            "metric": "encrypted-image inferences/s (FFConv MNIST-shaped HECNN, cfg2)",
+            "value": inf["images_per_s"], "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": inf["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded images)",
+            "config": {"workload": f"configs[2]: {args.images} images, chunks of {inf['chunk']}",
+                       "parallelism": f"dp{world} (image shards, no collective)"},
+            "inference": inf, "gpu_launches": inf["gpu_launches"], "clocks": inf["clocks"],
+            "e2e": {"value": inf["e2e_images_per_s"], "unit": "images/s",
+                    "h2d_bytes_per_step": inf["h2d_bytes_per_step"], "d2h_bytes_per_step": inf["d2h_bytes_per_step"]},
+        }
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+        return
     res = run_rotation(args, rank, world, local_rank)
+    if not args.no_inference:
+        # secondary line item: configs[2]-shaped inference on a bounded sample per GPU
+        inf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=1, warmup=1)
+        res["inference"] = inf
+        res["rates"]["images_per_s"] = inf["images_per_s"]
     if rank == 0 and world == 1:
         rate, sample = cpu_baseline_rotation(1, seconds=3.0)
         res["cpu_baseline"] = {"value": rate, "unit": "rotations/s", "cores": 1, "kind": "port",
                                "sample": sample,
                                "note": "reference slot-engine algorithm (np.roll), no cryptography"}
+        if not args.no_inference:
+            irate, isample = cpu_baseline_inference(1)
+            res["cpu_baseline_inference"] = {"value": irate, "unit": "images/s", "cores": 1, "kind": "port",
+                                             "sample": isample}
     if rank == 0:
         print(json.dumps(res), flush=True)
     if world > 1:

@@ -224,21 +224,37 @@ def _tensor(value, ctx):
     return None
 
 
+def pack_input(net: NetworkSpec, plan: PackingPlan, input_tensor, ctx):
+    """Client side of the plan's first step: encrypt the input(s) in the layout
+    the plan starts from (runner.py:342-352)."""
+    step = plan.steps[0]
+    x = np.asarray(input_tensor)
+    if step.op == PACK_DENSE:
+        return dense_pack(x, ctx)
+    if step.op == PACK_COLUMNS:
+        ow, oh = step.kernel.out_dims(step.in_shape)
+        return conv_pack(plain_im2col(x, step.kernel), ctx, (ow, oh))
+    raise ValueError(f"plan does not start with a packing step: {step.op}")
+
+
 def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input_tensor, *,
                   ctx=None, track_values: bool = True, capture_layers: bool = False,
-                  mask_fc: bool = True) -> RunResult:
+                  mask_fc: bool = True, packed=None, decrypt: bool = True) -> RunResult:
     """Walk the plan over an evaluation context (runner.py:290-409).
 
     input_tensor: (c, h, w) for a batch-1 context or (B, c, h, w).
     ctx: any object with the HeContext interface; default: a GPU HeContext on
-    net.scheme (its parameters must then be batching-compatible)."""
+    net.scheme (its parameters must then be batching-compatible).
+    packed: an already encrypted input (from pack_input); decrypt=False leaves
+    the logits encrypted (RunResult.value) -- together they bracket the
+    server-side evaluation only."""
     validate_weights(net, weights)
     if plan.net != net:
         raise ValueError("plan was built for a different network")
     if ctx is None:
         ctx = HeContext(net.scheme)
     x_in = None
-    if track_values:
+    if track_values and packed is None:
         x_in = np.asarray(input_tensor)
         shape = (net.input_shape.c, net.input_shape.h, net.input_shape.w)
         if x_in.shape[-3:] != shape:
@@ -250,7 +266,9 @@ def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input
         d_before = packed_depth(value) if value is not None else (0, 0)
         phases = None
         op = step.op
-        if op == PACK_DENSE:
+        if packed is not None and k == 0 and op in (PACK_DENSE, PACK_COLUMNS):
+            value = packed
+        elif op == PACK_DENSE:
             value = dense_pack(x_in if track_values else np.zeros((step.in_shape.c, step.in_shape.h,
                                                                    step.in_shape.w), dtype=np.int64),
                                ctx, tracked=track_values)
@@ -297,7 +315,7 @@ def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input
                                  "assembly_delta": d_after[1] - d_before[1]})
             if capture_layers and track_values:
                 layer_outputs.append((step.layer_index, _tensor(value, ctx)))
-    logits = _logits(value, ctx) if track_values else None
+    logits = _logits(value, ctx) if (track_values and decrypt) else None
     depth, adepth = packed_depth(value)
     return RunResult(logits, records, ctx.counters.copy(), depth, adepth, layer_depths, layer_outputs,
                      ctx.elided_rotations, value)
