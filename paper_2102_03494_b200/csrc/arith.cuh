@@ -46,6 +46,17 @@ DEV u64 mont(u64 a, u64 b, u64 q, u64 qinv) {
     u64 mh = mulhi(m, q);
     return hi >= mh ? hi - mh : hi - mh + q;
 }
+// Montgomery reduction of a 128-bit value T = (hi, lo) < q 2^64: T 2^-64 mod q
+DEV u64 mont_reduce(u64 hi, u64 lo, u64 q, u64 qinv) {
+    u64 m = lo * qinv;
+    u64 mh = mulhi(m, q);
+    return hi >= mh ? hi - mh : hi - mh + q;
+}
+DEV void mac128(u64 &hi, u64 &lo, u64 a, u64 b) {      // (hi, lo) += a * b
+    u64 pl = a * b, ph = mulhi(a, b);
+    lo += pl;
+    hi += ph + (lo < pl ? 1 : 0);
+}
 DEV u64 addm(u64 a, u64 b, u64 q) { u64 s = a + b; return s >= q ? s - q : s; }
 DEV u64 subm(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
 DEV u64 negm(u64 a, u64 q) { return a ? q - a : 0; }

@@ -136,9 +136,12 @@ struct fhe_ctx {
     u64 pinv[MAXQ]{}, pinv_sh[MAXQ]{};
     std::unordered_map<u32, KeyBuf> keys;
     u64 key_bytes = 0;
-    // workspaces
+    // workspaces (key switching: two ping-pong sets, one per stream)
     int S = 1;                          // key-switching sub-batch
-    u64 *w_D = nullptr, *w_C1 = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;
+    u64 *w_D = nullptr, *w_C1 = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;   // current set
+    u64 *ws_D[2]{}, *ws_C1[2]{}, *ws_Ext[2]{}, *ws_Acc[2]{};
+    cudaStream_t streams[2]{};
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     u64 *w_sq = nullptr;
     size_t w_sq_words = 0;
     u64 *w_tmp = nullptr;
@@ -209,11 +212,11 @@ static inline long long nblocks(long long total, int bs = 256) {
 static std::mutex g_attr_mu;
 static std::unordered_set<const void *> g_attr_done;
 
-template <int LOGN, typename... KArgs, typename... Args>
+template <int LOGN, bool INV = false, typename... KArgs, typename... Args>
 static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim3 grid, cudaStream_t st,
                        Args... args) {
     ProfScope ps_(c, name);
-    using C = NttCfg<LOGN>;
+    using C = NttCfg<LOGN, INV ? DefaultWInv<LOGN>::value : DefaultW<LOGN>::value>;
     const size_t smem = (size_t)C::SMEM_WORDS * sizeof(u64);
     {
         std::lock_guard<std::mutex> lk(g_attr_mu);
@@ -225,22 +228,22 @@ static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim
     kern<<<grid, C::TH, smem, st>>>(args...);
 }
 
-#define LOGN_SWITCH(logn, BODY)                \
-    switch (logn) {                            \
-        case 2: { constexpr int LG = 2; BODY; } break;   \
-        case 3: { constexpr int LG = 3; BODY; } break;   \
-        case 4: { constexpr int LG = 4; BODY; } break;   \
-        case 5: { constexpr int LG = 5; BODY; } break;   \
-        case 6: { constexpr int LG = 6; BODY; } break;   \
-        case 7: { constexpr int LG = 7; BODY; } break;   \
-        case 8: { constexpr int LG = 8; BODY; } break;   \
-        case 9: { constexpr int LG = 9; BODY; } break;   \
-        case 10: { constexpr int LG = 10; BODY; } break; \
-        case 11: { constexpr int LG = 11; BODY; } break; \
-        case 12: { constexpr int LG = 12; BODY; } break; \
-        case 13: { constexpr int LG = 13; BODY; } break; \
-        case 14: { constexpr int LG = 14; BODY; } break; \
-        default: break;                        \
+#define LOGN_SWITCH(logn, ...)                                   \
+    switch (logn) {                                              \
+        case 2: { constexpr int LG = 2; __VA_ARGS__; } break;    \
+        case 3: { constexpr int LG = 3; __VA_ARGS__; } break;    \
+        case 4: { constexpr int LG = 4; __VA_ARGS__; } break;    \
+        case 5: { constexpr int LG = 5; __VA_ARGS__; } break;    \
+        case 6: { constexpr int LG = 6; __VA_ARGS__; } break;    \
+        case 7: { constexpr int LG = 7; __VA_ARGS__; } break;    \
+        case 8: { constexpr int LG = 8; __VA_ARGS__; } break;    \
+        case 9: { constexpr int LG = 9; __VA_ARGS__; } break;    \
+        case 10: { constexpr int LG = 10; __VA_ARGS__; } break;  \
+        case 11: { constexpr int LG = 11; __VA_ARGS__; } break;  \
+        case 12: { constexpr int LG = 12; __VA_ARGS__; } break;  \
+        case 13: { constexpr int LG = 13; __VA_ARGS__; } break;  \
+        case 14: { constexpr int LG = 14; __VA_ARGS__; } break;  \
+        default: break;                                          \
     }
 
 static int ntt_rows(fhe_ctx *c, int rows, const NttRowsArgs &a, const char *name = "k_ntt_rows") {
@@ -251,7 +254,7 @@ static int ntt_rows(fhe_ctx *c, int rows, const NttRowsArgs &a, const char *name
 }
 static int intt_rows(fhe_ctx *c, int rows, const InttRowsArgs &a, const char *name = "k_intt_rows") {
     if (rows <= 0) return 0;
-    LOGN_SWITCH(c->logn, launch_row<LG>(c, name, k_intt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
+    LOGN_SWITCH(c->logn, launch_row<LG, true>(c, name, k_intt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
     CHECK_LAUNCH();
     return 0;
 }
@@ -304,6 +307,8 @@ static int validate(const fhe_params *p) {
     }
     for (u32 i = 0; i < p->L; i++)
         if (p->p[0] < p->q[i]) return fail(FHE_EINVAL, "special prime must exceed every q_i");
+    // the key-switching inner product accumulates L products < q^2 in 128 bits
+    if ((u128)p->p[0] * p->L >= ((u128)1 << 64)) return fail(FHE_EINVAL, "L * max modulus must stay below 2^64");
     return 0;
 }
 
@@ -488,10 +493,16 @@ static int setup_workspace(fhe_ctx *c) {
     if (S < 1) S = 1;
     if (S > MAXS) S = MAXS;
     c->S = S;
-    CU(cudaMalloc((void **)&c->w_D, S * L * n * 8));
-    CU(cudaMalloc((void **)&c->w_C1, S * L * n * 8));
-    CU(cudaMalloc((void **)&c->w_Ext, S * L * (L + 1) * n * 8));
-    CU(cudaMalloc((void **)&c->w_Acc, S * 2 * (L + 1) * n * 8));
+    for (int k = 0; k < 2; k++) {
+        CU(cudaMalloc((void **)&c->ws_D[k], S * L * n * 8));
+        CU(cudaMalloc((void **)&c->ws_C1[k], S * L * n * 8));
+        CU(cudaMalloc((void **)&c->ws_Ext[k], S * L * (L + 1) * n * 8));
+        CU(cudaMalloc((void **)&c->ws_Acc[k], S * 2 * (L + 1) * n * 8));
+    }
+    c->w_D = c->ws_D[0]; c->w_C1 = c->ws_C1[0]; c->w_Ext = c->ws_Ext[0]; c->w_Acc = c->ws_Acc[0];
+    CU(cudaStreamCreateWithFlags(&c->streams[1], cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     if (c->nb) {
         size_t l = L, nb = c->nb;
         c->w_sq_words = S * n * (2 * l + 2 * nb + 3 * (l + nb) + 3 * l + 3 * l);
@@ -518,6 +529,7 @@ extern "C" int fhe_ctx_create(const fhe_params *params, fhe_ctx **out) {
         if (cudaGetDeviceProperties(&prop, c->dev) != cudaSuccess) { rc = fail(FHE_EDEVICE, "no CUDA device"); break; }
         if (prop.major != 10) { rc = fail(FHE_EDEVICE, "device %s is sm_%d%d; this build targets sm_100a", prop.name, prop.major, prop.minor); break; }
         if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(FHE_EDEVICE, "stream creation failed"); break; }
+        c->streams[0] = c->st;
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, c->dev) == cudaSuccess) {
             u64 thresh = ~0ull;
@@ -563,8 +575,15 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto &kv : c->keys) cudaFree(kv.second.d);
     void *bufs[] = {c->d_mods, c->d_tw, c->d_s_can, c->d_s_m, c->d_s2_m, c->d_sk_ids, c->d_slot2ntt,
-                    c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_D, c->w_C1, c->w_Ext, c->w_Acc, c->w_sq};
+                    c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_sq};
     for (void *b : bufs) if (b) cudaFree(b);
+    for (int k = 0; k < 2; k++) {
+        void *wb[] = {c->ws_D[k], c->ws_C1[k], c->ws_Ext[k], c->ws_Acc[k]};
+        for (void *b : wb) if (b) cudaFree(b);
+    }
+    if (c->streams[1]) { cudaStreamSynchronize(c->streams[1]); cudaStreamDestroy(c->streams[1]); }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->w_tmp) cudaFreeAsync(c->w_tmp, c->st);
     if (c->st) { cudaStreamSynchronize(c->st); cudaStreamDestroy(c->st); }
     delete c;
@@ -634,6 +653,69 @@ extern "C" int fhe_prof_report(fhe_ctx *c, char *buf, uint32_t len) {
         buf[len - 1] = 0;
     }
     return 0;
+}
+
+template <int LOGN, int W>
+static int bench_variant(fhe_ctx *c, int inverse, u32 rows, u32 iters, const u64 *in, u64 *out, float *ms) {
+    using C = NttCfg<LOGN, W>;
+    const size_t smem = (size_t)C::SMEM_WORDS * 8;
+    auto kf = k_bench_fwd<LOGN, W>;
+    auto ki = k_bench_inv<LOGN, W>;
+    CU(cudaFuncSetAttribute((const void *)kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaFuncSetAttribute((const void *)ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (u32 it = 0; it < iters + 2; it++) {
+        if (it == 2) cudaEventRecord(e0, c->st);
+        if (inverse) ki<<<rows, C::TH, smem, c->st>>>(in, out, c->d_mods, 0);
+        else kf<<<rows, C::TH, smem, c->st>>>(in, out, c->d_mods, 0);
+    }
+    cudaEventRecord(e1, c->st);
+    CU(cudaEventSynchronize(e1));
+    CHECK_LAUNCH();
+    cudaEventElapsedTime(ms, e0, e1);
+    *ms /= iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return 0;
+}
+
+extern "C" int fhe_bench_ntt(fhe_ctx *c, int W, int inverse, uint32_t rows, uint32_t iters, float *ms,
+                             uint32_t *mismatch) {
+    if (c->logn != 14) return fail(FHE_EINVAL, "bench_ntt is instantiated for n = 2^14 only");
+    size_t n = c->n;
+    u64 *in, *ref, *out;
+    CU(cudaMalloc((void **)&in, rows * n * 8));
+    CU(cudaMalloc((void **)&ref, rows * n * 8));
+    CU(cudaMalloc((void **)&out, rows * n * 8));
+    std::vector<u64> h(rows * n);
+    u64 q = c->P.q[0], x = 0x9E3779B97F4A7C15ull;
+    for (auto &v : h) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = x % q; }
+    CU(cudaMemcpy(in, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    float dummy;
+    int rc = bench_variant<14, 4>(c, inverse, rows, 1, in, ref, &dummy);
+    if (!rc) {
+        switch (W) {
+            case 4: rc = bench_variant<14, 4>(c, inverse, rows, iters, in, out, ms); break;
+            case 5: rc = bench_variant<14, 5>(c, inverse, rows, iters, in, out, ms); break;
+            case 6: rc = bench_variant<14, 6>(c, inverse, rows, iters, in, out, ms); break;
+            default: rc = fail(FHE_EINVAL, "W must be in {3,4,5,6}");
+        }
+    }
+    if (!rc) {
+        std::vector<u64> a(rows * n), b(rows * n);
+        cudaMemcpy(a.data(), ref, a.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy(b.data(), out, b.size() * 8, cudaMemcpyDeviceToHost);
+        u32 bad = 0;
+        for (u32 r = 0; r < rows; r++)
+            if (memcmp(a.data() + r * n, b.data() + r * n, n * 8)) bad++;
+        *mismatch = bad;
+    }
+    cudaFree(in);
+    cudaFree(ref);
+    cudaFree(out);
+    return rc;
 }
 
 extern "C" int fhe_launch_count(fhe_ctx *c, uint64_t *out) {
@@ -913,7 +995,7 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const u64 *key, const DigitT
     LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_modup", k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
                                         c->d_mods));
     CHECK_LAUNCH();
-    long long tot = (long long)((S + 1) / 2) * (l + 1) * n;
+    long long tot = (long long)((S + KS_GROUP - 1) / KS_GROUP) * (l + 1) * n;
     {
         ProfScope ps_(c, "k_ks_inner");
         k_ks_inner<<<(unsigned)nblocks(tot), 256, 0, c->st>>>(c->w_Ext, dt, key, c->w_Acc, S, (int)l, L,
@@ -946,18 +1028,34 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const u64 *key, const DigitT
 }
 
 // rotate a list of physical ciphertexts (each [2][l][n]) by Galois element g
+static void use_lane(fhe_ctx *c, int k) {
+    c->st = c->streams[k];
+    c->w_D = c->ws_D[k]; c->w_C1 = c->ws_C1[k]; c->w_Ext = c->ws_Ext[k]; c->w_Acc = c->ws_Acc[k];
+}
+
+// rotate a list of physical ciphertexts (each [2][l][n]) by Galois element g.
+// Sub-batches alternate between two streams with their own workspaces so the
+// small-grid steps of one (ModDown INTT) overlap the next one's ModUp.
 static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std::vector<u64 *> &out, u32 l, u32 g) {
     const u64 *key;
     TRY(get_key(c, g, &key));
     size_t n = c->n;
-    for (size_t b0 = 0; b0 < in.size(); b0 += c->S) {
+    const bool two = in.size() > (size_t)c->S;
+    if (two) {
+        CU(cudaEventRecord(c->ev_fork, c->streams[0]));
+        CU(cudaStreamWaitEvent(c->streams[1], c->ev_fork, 0));
+    }
+    int rc = 0;
+    int lane = 0;
+    for (size_t b0 = 0; b0 < in.size() && !rc; b0 += c->S, lane ^= 1) {
+        use_lane(c, two ? lane : 0);
         int S = (int)std::min<size_t>(c->S, in.size() - b0);
         PtrTab pt;
         memset(&pt, 0, sizeof pt);
         for (int s = 0; s < S; s++) { pt.in[s] = in[b0 + s]; pt.out[s] = out[b0 + s]; }
-        LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rot_gather_intt", k_rot_gather_intt<LG>, dim3(S, l), c->st, pt,
-                                            (int)l, g, c->w_C1, c->w_D, c->d_mods));
-        CHECK_LAUNCH();
+        LOGN_SWITCH(c->logn, launch_row<LG, true>(c, "k_rot_gather_intt", k_rot_gather_intt<LG>, dim3(S, l), c->st,
+                                                  pt, (int)l, g, c->w_C1, c->w_D, c->d_mods));
+        if (cudaGetLastError() != cudaSuccess) { rc = fail(FHE_EDEVICE, "k_rot_gather_intt launch failed"); break; }
         DigitTab dt;
         KsOut ko;
         memset(&dt, 0, sizeof dt);
@@ -972,9 +1070,14 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
         ko.add_pstride = 0;
         ko.add_pmask = 1;
         ko.add_g = g;
-        TRY(keyswitch_core(c, S, l, key, dt, ko));
+        rc = keyswitch_core(c, S, l, key, dt, ko);
     }
-    return 0;
+    use_lane(c, 0);
+    if (two) {
+        CU(cudaEventRecord(c->ev_join, c->streams[1]));
+        CU(cudaStreamWaitEvent(c->streams[0], c->ev_join, 0));
+    }
+    return rc;
 }
 
 static int check_rot(fhe_ctx *c, u32 k) {

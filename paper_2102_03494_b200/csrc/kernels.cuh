@@ -66,8 +66,8 @@ struct NttRowsArgs {
 DEV long long row_off(int r, u32 rdiv, long long A, long long B) { return (long long)(r / rdiv) * A + (long long)(r % rdiv) * B; }
 
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_ntt_rows(NttRowsArgs a, const ModInfo *__restrict__ mods) {
-    using C = NttCfg<LOGN>;
+__global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_ntt_rows(NttRowsArgs a, const ModInfo *__restrict__ mods) {
+    using C = FwdCfg<LOGN>;
     extern __shared__ u64 sm[];
     const int r = blockIdx.x, tid = threadIdx.x;
     const ModInfo M = mods[a.map.id[(r / a.div) % a.period]];
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_ntt_rows(NttRowsArgs a, co
     ntt_fwd_core<LOGN>(v, sm, M, tid);
     u64 *dst = a.dst + row_off(r, a.rdiv, a.dA, a.dB);
     for (int i = tid; i < C::N; i += C::TH) {
-        u64 x = sm[spad(i)];
+        u64 x = sm[C::pad(i)];
         if (a.epi == 1) x = to_mont(x, M);
         else if (a.epi == 2) x = addm(dst[i], x, M.q);
         dst[i] = x;
@@ -112,26 +112,26 @@ struct InttRowsArgs {
 };
 
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_intt_rows(InttRowsArgs a, const ModInfo *__restrict__ mods) {
-    using C = NttCfg<LOGN>;
+__global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_intt_rows(InttRowsArgs a, const ModInfo *__restrict__ mods) {
+    using C = InvCfg<LOGN>;
     extern __shared__ u64 sm[];
     const int r = blockIdx.x, tid = threadIdx.x;
     const ModInfo M = mods[a.map.id[(r / a.div) % a.period]];
     const u64 *src = a.src + row_off(r, a.rdiv, a.sA, a.sB);
     if (a.gather == 2) {
-        for (int i = tid; i < C::N; i += C::TH) sm[spad(i)] = src[i];
+        for (int i = tid; i < C::N; i += C::TH) sm[C::pad(i)] = src[i];
         __syncthreads();
         u64 w[C::E];
 #pragma unroll
-        for (int e = 0; e < C::E; e++) w[e] = sm[spad(galois_perm(tid + e * C::TH, a.g, LOGN))];
+        for (int e = 0; e < C::E; e++) w[e] = sm[C::pad(galois_perm(tid + e * C::TH, a.g, LOGN))];
         __syncthreads();
 #pragma unroll
-        for (int e = 0; e < C::E; e++) sm[spad(tid + e * C::TH)] = w[e];
+        for (int e = 0; e < C::E; e++) sm[C::pad(tid + e * C::TH)] = w[e];
     } else {
         for (int i = tid; i < C::N; i += C::TH) {
             u64 x = a.gather == 1 ? src[a.tab[i]] : src[i];
             if (a.reduce) x = red64(x, M.q, M.mu);
-            sm[spad(i)] = x;
+            sm[C::pad(i)] = x;
         }
     }
     __syncthreads();
@@ -152,17 +152,17 @@ struct PtrTab {
 // gather on the way out (C1p[s][i]: NTT-form digit for the inner-product
 // diagonal) and on the first inverse-NTT pass (D[s][i]: coefficient digit).
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt, int l, u32 g, u64 *C1p, u64 *D,
+__global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt, int l, u32 g, u64 *C1p, u64 *D,
                                                                   const ModInfo *__restrict__ mods) {
-    using C = NttCfg<LOGN>;
+    using C = InvCfg<LOGN>;
     extern __shared__ u64 sm[];
     const int s = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
     const long long n = C::N;
     const u64 *src = pt.in[s] + ((long long)l + i) * n;
-    for (int x = tid; x < C::N; x += C::TH) sm[spad(x)] = src[x];
+    for (int x = tid; x < C::N; x += C::TH) sm[C::pad(x)] = src[x];
     __syncthreads();
     u64 *side = C1p + ((long long)s * l + i) * n;
-    for (int x = tid; x < C::N; x += C::TH) side[x] = sm[spad(galois_perm(x, g, LOGN))];
+    for (int x = tid; x < C::N; x += C::TH) side[x] = sm[C::pad(galois_perm(x, g, LOGN))];
     const ModInfo M = mods[i];
     u64 v[C::E];
     ntt_inv_core<LOGN>(v, sm, M, tid, g);
@@ -180,9 +180,9 @@ struct DigitTab {
 // prime i (i == l: the special prime) and transformed; the diagonal i == j is
 // skipped (the inner product reads it from DigitTab.ntt).
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
+__global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
                                                         const ModInfo *__restrict__ mods) {
-    using C = NttCfg<LOGN>;
+    using C = FwdCfg<LOGN>;
     extern __shared__ u64 sm[];
     const int s = blockIdx.x, j = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
     if (i == j) return;
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_modup(DigitTab dt, u64 *Ex
     for (int e = 0; e < C::E; e++) v[e] = red64(src[(e << (LOGN - C::W)) | tid], M.q, M.mu);
     ntt_fwd_core<LOGN>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n;
-    for (int x = tid; x < C::N; x += C::TH) dst[x] = sm[spad(x)];
+    for (int x = tid; x < C::N; x += C::TH) dst[x] = sm[C::pad(x)];
 }
 
 // Rescale by a dropped prime (ModDown over the special prime, or BFV modulus
@@ -214,8 +214,8 @@ struct RescaleArgs {
 };
 
 template <int LOGN>
-__global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
-    using C = NttCfg<LOGN>;
+__global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
+    using C = FwdCfg<LOGN>;
     extern __shared__ u64 sm[];
     const int s = blockIdx.x, p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
     const long long n = C::N;
@@ -235,16 +235,16 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
 #pragma unroll
     for (int e = 0; e < C::E; e++) {
         const int x = tid + e * C::TH;
-        y[e] = shoup(subm(base[x], sm[spad(x)], M.q), f, fsh, M.q);
+        y[e] = shoup(subm(base[x], sm[C::pad(x)], M.q), f, fsh, M.q);
     }
     if (add && a.add_g) {
         __syncthreads();
-        for (int x = tid; x < C::N; x += C::TH) sm[spad(x)] = add[x];
+        for (int x = tid; x < C::N; x += C::TH) sm[C::pad(x)] = add[x];
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < C::E; e++) {
             const int x = tid + e * C::TH;
-            y[e] = addm(y[e], sm[spad(galois_perm(x, a.add_g, LOGN))], M.q);
+            y[e] = addm(y[e], sm[C::pad(galois_perm(x, a.add_g, LOGN))], M.q);
         }
     } else if (add) {
 #pragma unroll
@@ -261,41 +261,41 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
 
 // Key switching, step 3: acc_p[s][i] = sum_j Ext[s][j][i] * key_p[j][i]; keys in
 // Montgomery form, layout [L digits][2][L+1 primes][n].  One thread per
-// (pair of cts, prime i, coefficient x): each key word feeds two ciphertexts.
+// (group of 4 cts, prime i, coefficient x): the 2l key words are loaded once and
+// reused 4 times; products accumulate in 128 bits and are Montgomery-reduced
+// once per output (sum of l products < l q^2 < q 2^64 for l q < 2^64).
+#define KS_GROUP 4
 __global__ void k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, const u64 *__restrict__ key,
                            u64 *__restrict__ Acc, int S, int l, int L, int logn, int special_id,
                            const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
-    const int pairs = (S + 1) / 2;
-    GRID_STRIDE(idx, (long long)pairs * (l + 1) * n) {
+    const int groups = (S + KS_GROUP - 1) / KS_GROUP;
+    GRID_STRIDE(idx, (long long)groups * (l + 1) * n) {
         const long long x = idx & (n - 1);
         const long long r = idx >> logn;
         const int i = (int)(r % (l + 1));
-        const int s0 = 2 * (int)(r / (l + 1));
-        const bool two = s0 + 1 < S;
+        const int s0 = KS_GROUP * (int)(r / (l + 1));
         const int kp = i == l ? L : i;
         const ModInfo &M = mods[i == l ? special_id : i];
         const u64 q = M.q, qi = M.qinv;
-        u64 a00 = 0, a01 = 0, a10 = 0, a11 = 0;
+        u64 kb[MAXQ], ka[MAXQ];
         for (int j = 0; j < l; j++) {
-            const u64 kb = __ldg(key + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
-            const u64 ka = __ldg(key + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
-            const u64 e0 = i == j ? dt.ntt[s0][(long long)j * n + x]
-                                  : Ext[((((long long)s0 * l + j) * (l + 1)) + i) * n + x];
-            a00 = addm(a00, mont(e0, kb, q, qi), q);
-            a01 = addm(a01, mont(e0, ka, q, qi), q);
-            if (two) {
-                const u64 e1 = i == j ? dt.ntt[s0 + 1][(long long)j * n + x]
-                                      : Ext[((((long long)(s0 + 1) * l + j) * (l + 1)) + i) * n + x];
-                a10 = addm(a10, mont(e1, kb, q, qi), q);
-                a11 = addm(a11, mont(e1, ka, q, qi), q);
-            }
+            kb[j] = __ldg(key + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
+            ka[j] = __ldg(key + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
         }
-        Acc[(((long long)s0 * 2 + 0) * (l + 1) + i) * n + x] = a00;
-        Acc[(((long long)s0 * 2 + 1) * (l + 1) + i) * n + x] = a01;
-        if (two) {
-            Acc[(((long long)(s0 + 1) * 2 + 0) * (l + 1) + i) * n + x] = a10;
-            Acc[(((long long)(s0 + 1) * 2 + 1) * (l + 1) + i) * n + x] = a11;
+#pragma unroll
+        for (int u = 0; u < KS_GROUP; u++) {
+            const int s = s0 + u;
+            if (s >= S) break;
+            u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+            for (int j = 0; j < l; j++) {
+                const u64 e = i == j ? dt.ntt[s][(long long)j * n + x]
+                                     : Ext[((((long long)s * l + j) * (l + 1)) + i) * n + x];
+                mac128(h0, l0, e, kb[j]);
+                mac128(h1, l1, e, ka[j]);
+            }
+            Acc[(((long long)s * 2 + 0) * (l + 1) + i) * n + x] = mont_reduce(h0, l0, q, qi);
+            Acc[(((long long)s * 2 + 1) * (l + 1) + i) * n + x] = mont_reduce(h1, l1, q, qi);
         }
     }
 }
@@ -637,4 +637,38 @@ __global__ void k_peak_modmul(u64 *sink, u32 iters, u64 q, u64 w, u64 wsh) {
 #pragma unroll
     for (int k = 0; k < 8; k++) acc ^= x[k];
     if (acc == 0x1234567ull) sink[0] = acc;
+}
+
+// ---------------------------------------------------------------- diagnostics
+// NTT core variants for the development benchmark (fhe_bench_ntt): one row per
+// CTA, coalesced load, core, coalesced store.
+template <int LOGN, int W>
+__global__ void __launch_bounds__(NttCfg<LOGN, W>::TH) k_bench_fwd(const u64 *in, u64 *out, const ModInfo *mods, int mid) {
+    using C = NttCfg<LOGN, W>;
+    extern __shared__ u64 sm[];
+    const int tid = threadIdx.x;
+    const ModInfo M = mods[mid];
+    const u64 *src = in + (long long)blockIdx.x * C::N;
+    u64 v[C::E];
+#pragma unroll
+    for (int e = 0; e < C::E; e++) v[e] = src[(e << (LOGN - C::W)) | tid];
+    ntt_fwd_core<LOGN, W>(v, sm, M, tid);
+    u64 *dst = out + (long long)blockIdx.x * C::N;
+    for (int i = tid; i < C::N; i += C::TH) dst[i] = sm[C::pad(i)];
+}
+
+template <int LOGN, int W>
+__global__ void __launch_bounds__(NttCfg<LOGN, W>::TH) k_bench_inv(const u64 *in, u64 *out, const ModInfo *mods, int mid) {
+    using C = NttCfg<LOGN, W>;
+    extern __shared__ u64 sm[];
+    const int tid = threadIdx.x;
+    const ModInfo M = mods[mid];
+    const u64 *src = in + (long long)blockIdx.x * C::N;
+    for (int i = tid; i < C::N; i += C::TH) sm[C::pad(i)] = src[i];
+    __syncthreads();
+    u64 v[C::E];
+    ntt_inv_core<LOGN, W>(v, sm, M, tid);
+    u64 *dst = out + (long long)blockIdx.x * C::N;
+#pragma unroll
+    for (int e = 0; e < C::E; e++) dst[(e << (LOGN - C::W)) | tid] = v[e];
 }

@@ -5,25 +5,49 @@
 // bit-reversed evaluations -> natural coefficients, scaled by n^-1.  Same
 // ordering and twiddles (minimal primitive 2n-th root) as oracle/golden_rlwe.c.
 //
-// Layout: every thread owns E = 16 words in registers and runs up to 4
-// butterfly stages per pass (radix-16); passes exchange through shared memory
-// padded one word per 16 (conflict-free for 64-bit accesses).  n = 2^14 uses
-// 1024 threads and 136 KB of shared memory.  Values are kept lazily in [0, 4q)
+// Layout: every thread owns E = 2^W words in registers and runs up to W
+// butterfly stages per pass; passes exchange through shared memory padded one
+// word per 2^W (conflict-free for 64-bit accesses).  n >= 2^12 uses W = 5
+// (radix-32, 512 threads x 128 registers for n = 2^14, 132 KB of shared memory)
+// for inverse transforms, W = 4 (1024 x 64) for forward ones: standalone 46 % / 40 %
+// of the integer peak (fwd W5 / inv W5) vs 45 % / 35 % at W = 4, but the fused
+// forward kernels (ModUp, rescale) run faster at W = 4 (profiles/r01_*).  Values are kept lazily in [0, 4q)
 // (forward, Harvey) / [0, 2q) (inverse) and reduced once at the end.
 #pragma once
 #include "arith.cuh"
 
+#ifndef NTT_W_FWD
+#define NTT_W_FWD 4
+#endif
+#ifndef NTT_W_INV
+#define NTT_W_INV 5
+#endif
+
+// default radix per pass: 2^5 (512 threads, 32 words each) for the large rings,
+// 2^4 below; overridable for experiments (csrc/ntt_bench.cu)
 template <int LOGN>
+struct DefaultW {      // forward transforms
+    static constexpr int value = LOGN < 4 ? LOGN : (LOGN >= 12 ? NTT_W_FWD : 4);
+};
+template <int LOGN>
+struct DefaultWInv {   // inverse transforms
+    static constexpr int value = LOGN < 4 ? LOGN : (LOGN >= 12 ? NTT_W_INV : 4);
+};
+
+
+template <int LOGN, int WW = DefaultW<LOGN>::value>
 struct NttCfg {
     static constexpr int N = 1 << LOGN;
-    static constexpr int W = LOGN < 4 ? LOGN : 4;      // stages per pass
+    static constexpr int W = WW;                        // stages per pass
     static constexpr int E = 1 << W;                    // words per thread
     static constexpr int TH = N / E;                    // threads per row
     static constexpr int NP = (LOGN + W - 1) / W;       // passes
-    static constexpr int SMEM_WORDS = N + (N >> 4) + 1;
+    static constexpr int SMEM_WORDS = N + (N >> W) + 1;
+    // one pad word per 2^W: every pass's access pattern is conflict-free for 64-bit words
+    static DEV int pad(int i) { return i + (i >> W); }
 };
-
-DEV int spad(int i) { return i + (i >> 4); }
+template <int LOGN> using FwdCfg = NttCfg<LOGN, DefaultW<LOGN>::value>;
+template <int LOGN> using InvCfg = NttCfg<LOGN, DefaultWInv<LOGN>::value>;
 
 // insert the W bits of e at bit position f0 of the thread index
 template <int W>
@@ -33,11 +57,11 @@ DEV int fidx(int tid, int e, int f0) {
 }
 
 // Forward. In: v[] holds element fidx(tid, e, LOGN - W) (i.e. v[e] = a[(e << (LOGN-W)) | tid])
-// with values < 4q.  Out: canonical values in sm[spad(i)], bit-reversed order; ends
+// with values < 4q.  Out: canonical values in sm[C::pad(i)], bit-reversed order; ends
 // with __syncthreads().
-template <int LOGN>
-DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int tid) {
-    using C = NttCfg<LOGN>;
+template <int LOGN, int WW = DefaultW<LOGN>::value>
+DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid) {
+    using C = NttCfg<LOGN, WW>;
     constexpr int W = C::W, E = C::E, NP = C::NP;
     const u64 q = M.q, q2 = 2 * q;
 #pragma unroll
@@ -47,7 +71,7 @@ DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int 
         const int k = (LOGN - s0) < W ? (LOGN - s0) : W;
         if (p > 0) {
 #pragma unroll
-            for (int e = 0; e < E; e++) v[e] = sm[spad(fidx<W>(tid, e, f0))];
+            for (int e = 0; e < E; e++) v[e] = sm[C::pad(fidx<W>(tid, e, f0))];
             __syncthreads();
         }
 #pragma unroll
@@ -77,17 +101,17 @@ DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int 
             }
         }
 #pragma unroll
-        for (int e = 0; e < E; e++) sm[spad(fidx<W>(tid, e, f0))] = v[e];
+        for (int e = 0; e < E; e++) sm[C::pad(fidx<W>(tid, e, f0))] = v[e];
         __syncthreads();
     }
 }
 
-// Inverse. In: canonical (or < 2q) values in sm[spad(i)], bit-reversed order, synced.
+// Inverse. In: canonical (or < 2q) values in sm[C::pad(i)], bit-reversed order, synced.
 // Out: v[e] = a[(e << (LOGN-W)) | tid] canonical, scaled by n^-1.  Shared memory is
 // free for reuse only after a __syncthreads() by the caller.
-template <int LOGN>
-DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int tid, u32 g_perm = 0) {
-    using C = NttCfg<LOGN>;
+template <int LOGN, int WW = DefaultWInv<LOGN>::value>
+DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid, u32 g_perm = 0) {
+    using C = NttCfg<LOGN, WW>;
     constexpr int W = C::W, E = C::E, NP = C::NP, N = C::N;
     const u64 q = M.q, q2 = 2 * q;
 #pragma unroll
@@ -97,10 +121,10 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int 
         const int k = (LOGN - lt0) < W ? (LOGN - lt0) : W;
         if (p == 0 && g_perm) {
 #pragma unroll
-            for (int e = 0; e < E; e++) v[e] = sm[spad(galois_perm(fidx<W>(tid, e, f0), g_perm, LOGN))];
+            for (int e = 0; e < E; e++) v[e] = sm[C::pad(galois_perm(fidx<W>(tid, e, f0), g_perm, LOGN))];
         } else {
 #pragma unroll
-            for (int e = 0; e < E; e++) v[e] = sm[spad(fidx<W>(tid, e, f0))];
+            for (int e = 0; e < E; e++) v[e] = sm[C::pad(fidx<W>(tid, e, f0))];
         }
         if (p < NP - 1) __syncthreads();
 #pragma unroll
@@ -123,7 +147,7 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN>::E], u64 *sm, const ModInfo &M, int 
         }
         if (p < NP - 1) {
 #pragma unroll
-            for (int e = 0; e < E; e++) sm[spad(fidx<W>(tid, e, f0))] = v[e];
+            for (int e = 0; e < E; e++) sm[C::pad(fidx<W>(tid, e, f0))] = v[e];
             __syncthreads();
         }
     }
