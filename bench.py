@@ -424,6 +424,13 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
         t = torch.tensor([e2e_s], device=f"cuda:{local_rank}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # per-kernel breakdown of one chunk (single-stream, isolated kernel times)
+    lib.call("fhe_prof_enable", ev.ctx, 1)
+    evaluate(packed[:1])
+    buf = ctypes.create_string_buffer(1 << 16)
+    lib.call("fhe_prof_report", ev.ctx, buf, len(buf))
+    lib.call("fhe_prof_enable", ev.ctx, 0)
+    breakdown = {k: {"calls": c, "ms": round(m, 3)} for k, (c, m) in parse_prof(buf.value.decode()).items()}
     # physical ciphertext rotations: logical rotations x CRT primes x row pairs
     phys_rot = rots * rp.T * ctx.rows
     mm = phys_rot * rotation_modmuls(rp.n, rp.L)
@@ -439,6 +446,7 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
         "gpu_launches": int(cnt1.value - cnt0.value),
         "h2d_bytes_per_step": int(xs.size * 8 * world), "d2h_bytes_per_step": int(10 * images_total * 8 * rp.T),
         "clocks": clk.summary(), "logits_sample": [str(int(v)) for v in np.asarray(logits[0])[0][:3]],
+        "kernel_ms_one_chunk": breakdown,
     }
 
 

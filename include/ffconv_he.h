@@ -142,6 +142,11 @@ int fhe_square(fhe_ctx *ctx, const fhe_ct *a, fhe_ct *out);
 
 /* batched forms: m independent operations in one launch sequence */
 int fhe_rotate_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k);
+/* out[i] = a[i] + rotate(a[i], k): one rotate-and-sum level, the addition fused
+ * into the key-switching epilogue */
+int fhe_rotate_add_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k);
+/* m rotations with their own steps k[i] in [1, N) (e.g. a combine chain) */
+int fhe_rotate_multi(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, const uint32_t *k, uint32_t m);
 int fhe_mul_plain_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m);
 int fhe_add_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *b, fhe_ct *const *out, uint32_t m);
 

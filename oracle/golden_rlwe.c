@@ -1037,6 +1037,19 @@ int fhe_rotate_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32_t m
     for (u32 i = 0; i < m; i++) { int rc = fhe_rotate(c, a[i], k, out[i]); if (rc) return rc; }
     return 0;
 }
+int fhe_rotate_add_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k) {
+    for (u32 i = 0; i < m; i++) {
+        int rc = fhe_rotate(c, a[i], k, out[i]);
+        if (rc) return rc;
+        rc = fhe_add(c, a[i], out[i], out[i]);
+        if (rc) return rc;
+    }
+    return 0;
+}
+int fhe_rotate_multi(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, const uint32_t *k, uint32_t m) {
+    for (u32 i = 0; i < m; i++) { int rc = fhe_rotate(c, a[i], k[i], out[i]); if (rc) return rc; }
+    return 0;
+}
 int fhe_mul_plain_many(fhe_ctx *c, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m) {
     for (u32 i = 0; i < m; i++) { int rc = fhe_mul_plain(c, a[i], pt[i], out[i]); if (rc) return rc; }
     return 0;

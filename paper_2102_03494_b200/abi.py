@@ -81,6 +81,8 @@ SIGNATURES = {
     "fhe_mod_switch": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fhe_square": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fhe_rotate_many": (c_int, [c_void_p, _VPP, _VPP, c_uint32, c_uint32]),
+    "fhe_rotate_multi": (c_int, [c_void_p, _VPP, _VPP, POINTER(c_uint32), c_uint32]),
+    "fhe_rotate_add_many": (c_int, [c_void_p, _VPP, _VPP, c_uint32, c_uint32]),
     "fhe_mul_plain_many": (c_int, [c_void_p, _VPP, _VPP, _VPP, c_uint32]),
     "fhe_add_many": (c_int, [c_void_p, _VPP, _VPP, _VPP, c_uint32]),
 }

@@ -985,10 +985,12 @@ struct KsOut {
     const u64 *add[MAXS];
     long long out_pstride, add_pstride;
     int add_pmask;
-    u32 add_g;
+    u32 add_g[MAXS];
+    const u64 *acc[MAXS];      // rotate-and-add: the input ct, added to both polys
+    long long acc_pstride;
 };
 
-static int keyswitch_core(fhe_ctx *c, int S, u32 l, const u64 *key, const DigitTab &dt, const KsOut &ko) {
+static int keyswitch_core(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsOut &ko) {
     size_t n = c->n;
     int L = (int)c->L;
     // ModUp: every off-diagonal (digit, prime) pair
@@ -998,8 +1000,16 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const u64 *key, const DigitT
     long long tot = (long long)((S + KS_GROUP - 1) / KS_GROUP) * (l + 1) * n;
     {
         ProfScope ps_(c, "k_ks_inner");
-        k_ks_inner<<<(unsigned)nblocks(tot), 256, 0, c->st>>>(c->w_Ext, dt, key, c->w_Acc, S, (int)l, L,
-                                                               (int)c->logn, c->special_id, c->d_mods);
+        const unsigned nb = (unsigned)nblocks(tot);
+#define KS_CASE(LLV) case LLV: k_ks_inner<LLV><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, (int)c->logn, \
+                                                                       c->special_id, c->d_mods); break;
+        switch (l) {
+            KS_CASE(1) KS_CASE(2) KS_CASE(3) KS_CASE(4) KS_CASE(5) KS_CASE(6) KS_CASE(7) KS_CASE(8)
+            KS_CASE(9) KS_CASE(10) KS_CASE(11) KS_CASE(12) KS_CASE(13) KS_CASE(14) KS_CASE(15) KS_CASE(16)
+            KS_CASE(17) KS_CASE(18) KS_CASE(19) KS_CASE(20) KS_CASE(21) KS_CASE(22) KS_CASE(23) KS_CASE(24)
+            default: return fail(FHE_EINVAL, "level %u unsupported by k_ks_inner", l);
+        }
+#undef KS_CASE
     }
     CHECK_LAUNCH();
     // ModDown: INTT of the special limb of both accumulators
@@ -1019,7 +1029,8 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const u64 *key, const DigitT
     ra.out_pstride = ko.out_pstride;
     ra.add_pstride = ko.add_pstride;
     ra.add_pmask = ko.add_pmask;
-    ra.add_g = ko.add_g;
+    for (int s = 0; s < S; s++) { ra.add_g[s] = ko.add_g[s]; ra.acc[s] = ko.acc[s]; }
+    ra.acc_pstride = ko.acc_pstride;
     ra.src_id = c->special_id;
     for (u32 i = 0; i < l; i++) { ra.fac[i] = c->pinv[i]; ra.fac_sh[i] = c->pinv_sh[i]; }
     LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
@@ -1033,28 +1044,37 @@ static void use_lane(fhe_ctx *c, int k) {
     c->w_D = c->ws_D[k]; c->w_C1 = c->ws_C1[k]; c->w_Ext = c->ws_Ext[k]; c->w_Acc = c->ws_Acc[k];
 }
 
-// rotate a list of physical ciphertexts (each [2][l][n]) by Galois element g.
-// Sub-batches alternate between two streams with their own workspaces so the
-// small-grid steps of one (ModDown INTT) overlap the next one's ModUp.
-static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std::vector<u64 *> &out, u32 l, u32 g) {
-    const u64 *key;
-    TRY(get_key(c, g, &key));
+// rotate a list of physical ciphertexts (each [2][l][n]), ciphertext i by
+// Galois element g[i].  Sub-batches alternate between two streams with their
+// own workspaces so the small-grid steps of one (ModDown INTT) overlap the
+// next one's ModUp.
+static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std::vector<u64 *> &out, u32 l,
+                       const std::vector<u32> &g, bool add_input = false) {
+    std::vector<const u64 *> keys(in.size());
+    for (size_t i = 0; i < in.size(); i++) {
+        if (i > 0 && g[i] == g[i - 1]) { keys[i] = keys[i - 1]; continue; }
+        TRY(get_key(c, g[i], &keys[i]));
+    }
     size_t n = c->n;
-    const bool two = in.size() > (size_t)c->S;
+    // (profiling runs single-stream so every kernel is timed in isolation)
+    const bool two = in.size() > (size_t)c->S && !c->prof;
+    // balanced sub-batches: ceil(count / ceil(count / S)) instead of S + remainder
+    const size_t nsub = (in.size() + c->S - 1) / c->S;
+    const size_t SB = (in.size() + nsub - 1) / nsub;
     if (two) {
         CU(cudaEventRecord(c->ev_fork, c->streams[0]));
         CU(cudaStreamWaitEvent(c->streams[1], c->ev_fork, 0));
     }
     int rc = 0;
     int lane = 0;
-    for (size_t b0 = 0; b0 < in.size() && !rc; b0 += c->S, lane ^= 1) {
+    for (size_t b0 = 0; b0 < in.size() && !rc; b0 += SB, lane ^= 1) {
         use_lane(c, two ? lane : 0);
-        int S = (int)std::min<size_t>(c->S, in.size() - b0);
+        int S = (int)std::min<size_t>(SB, in.size() - b0);
         PtrTab pt;
         memset(&pt, 0, sizeof pt);
-        for (int s = 0; s < S; s++) { pt.in[s] = in[b0 + s]; pt.out[s] = out[b0 + s]; }
+        for (int s = 0; s < S; s++) { pt.in[s] = in[b0 + s]; pt.out[s] = out[b0 + s]; pt.g[s] = g[b0 + s]; }
         LOGN_SWITCH(c->logn, launch_row<LG, true>(c, "k_rot_gather_intt", k_rot_gather_intt<LG>, dim3(S, l), c->st,
-                                                  pt, (int)l, g, c->w_C1, c->w_D, c->d_mods));
+                                                  pt, (int)l, c->w_C1, c->w_D, c->d_mods));
         if (cudaGetLastError() != cudaSuccess) { rc = fail(FHE_EDEVICE, "k_rot_gather_intt launch failed"); break; }
         DigitTab dt;
         KsOut ko;
@@ -1063,14 +1083,17 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
         for (int s = 0; s < S; s++) {
             dt.coef[s] = c->w_D + (size_t)s * l * n;
             dt.ntt[s] = c->w_C1 + (size_t)s * l * n;
+            dt.key[s] = keys[b0 + s];
             ko.out[s] = out[b0 + s];
             ko.add[s] = in[b0 + s];          // c0 limbs, read through the automorphism
+            ko.add_g[s] = g[b0 + s];
+            ko.acc[s] = add_input ? in[b0 + s] : nullptr;
         }
+        ko.acc_pstride = (long long)l * n;
         ko.out_pstride = (long long)l * n;
         ko.add_pstride = 0;
         ko.add_pmask = 1;
-        ko.add_g = g;
-        rc = keyswitch_core(c, S, l, key, dt, ko);
+        rc = keyswitch_core(c, S, l, dt, ko);
     }
     use_lane(c, 0);
     if (two) {
@@ -1093,7 +1116,7 @@ extern "C" int fhe_rotate(fhe_ctx *c, const fhe_ct *a, uint32_t k, fhe_ct *out) 
     std::vector<u64 *> o;
     size_t stride = 2ull * a->level * c->n;
     for (u32 ci = 0; ci < a->count; ci++) { in.push_back(a->d + ci * stride); o.push_back(out->d + ci * stride); }
-    return rotate_phys(c, in, o, a->level, galois_elt(c, k));
+    return rotate_phys(c, in, o, a->level, std::vector<u32>(in.size(), galois_elt(c, k)));
 }
 
 extern "C" int fhe_rotate_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k) {
@@ -1108,7 +1131,43 @@ extern "C" int fhe_rotate_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out,
         size_t stride = 2ull * l * c->n;
         for (u32 ci = 0; ci < a[h]->count; ci++) { in.push_back(a[h]->d + ci * stride); o.push_back(out[h]->d + ci * stride); }
     }
-    return rotate_phys(c, in, o, l, galois_elt(c, k));
+    return rotate_phys(c, in, o, l, std::vector<u32>(in.size(), galois_elt(c, k)));
+}
+
+extern "C" int fhe_rotate_add_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k) {
+    TRY(check_rot(c, k));
+    if (!m) return 0;
+    u32 l = a[0]->level;
+    std::vector<const u64 *> in;
+    std::vector<u64 *> o;
+    for (u32 h = 0; h < m; h++) {
+        if (a[h]->level != l || !same_shape(a[h], out[h])) return fail(FHE_ELEVEL, "rotate_add_many: shape/level mismatch");
+        if (a[h]->d == out[h]->d) return fail(FHE_EINVAL, "rotate_add_many: out must not alias the input");
+        size_t stride = 2ull * l * c->n;
+        for (u32 ci = 0; ci < a[h]->count; ci++) { in.push_back(a[h]->d + ci * stride); o.push_back(out[h]->d + ci * stride); }
+    }
+    return rotate_phys(c, in, o, l, std::vector<u32>(in.size(), galois_elt(c, k)), true);
+}
+
+extern "C" int fhe_rotate_multi(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, const uint32_t *k, uint32_t m) {
+    if (!m) return 0;
+    u32 l = a[0]->level;
+    std::vector<const u64 *> in;
+    std::vector<u64 *> o;
+    std::vector<u32> g;
+    for (u32 h = 0; h < m; h++) {
+        TRY(check_rot(c, k[h]));
+        if (a[h]->level != l || !same_shape(a[h], out[h])) return fail(FHE_ELEVEL, "rotate_multi: shape/level mismatch");
+        if (a[h]->d == out[h]->d) return fail(FHE_EINVAL, "rotate_multi: out must not alias the input");
+        size_t stride = 2ull * l * c->n;
+        u32 gh = galois_elt(c, k[h]);
+        for (u32 ci = 0; ci < a[h]->count; ci++) {
+            in.push_back(a[h]->d + ci * stride);
+            o.push_back(out[h]->d + ci * stride);
+            g.push_back(gh);
+        }
+    }
+    return rotate_phys(c, in, o, l, g);
 }
 
 extern "C" int fhe_mul_plain_many(fhe_ctx *c, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m) {
@@ -1209,13 +1268,14 @@ extern "C" int fhe_square(fhe_ctx *c, const fhe_ct *a, fhe_ct *out) {
         for (int s = 0; s < S; s++) {
             dt.coef[s] = E + ((size_t)s * 3 + 2) * l * n;
             dt.ntt[s] = En + ((size_t)s * 3 + 2) * l * n;
+            dt.key[s] = rk;
             ko.out[s] = out->d + (b0 + s) * 2 * l * n;
             ko.add[s] = En + (size_t)s * 3 * l * n;
         }
         ko.out_pstride = (long long)l * n;
         ko.add_pstride = (long long)l * n;
         ko.add_pmask = 3;
-        TRY(keyswitch_core(c, S, (u32)l, rk, dt, ko));
+        TRY(keyswitch_core(c, S, (u32)l, dt, ko));
     }
     return 0;
 }

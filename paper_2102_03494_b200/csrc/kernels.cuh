@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_intt_rows(InttRowsArgs a, 
 struct PtrTab {
     const u64 *in[MAXS];
     u64 *out[MAXS];
+    u32 g[MAXS];          // Galois element per ciphertext
 };
 
 // Key switching, step 1 (rotation).  grid (S, l): c1 limb i of input ct s.
@@ -152,12 +153,13 @@ struct PtrTab {
 // gather on the way out (C1p[s][i]: NTT-form digit for the inner-product
 // diagonal) and on the first inverse-NTT pass (D[s][i]: coefficient digit).
 template <int LOGN>
-__global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt, int l, u32 g, u64 *C1p, u64 *D,
+__global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt, int l, u64 *C1p, u64 *D,
                                                                   const ModInfo *__restrict__ mods) {
     using C = InvCfg<LOGN>;
     extern __shared__ u64 sm[];
     const int s = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
     const long long n = C::N;
+    const u32 g = pt.g[s];
     const u64 *src = pt.in[s] + ((long long)l + i) * n;
     for (int x = tid; x < C::N; x += C::TH) sm[C::pad(x)] = src[x];
     __syncthreads();
@@ -174,6 +176,7 @@ __global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt,
 struct DigitTab {
     const u64 *coef[MAXS];   // digit j of ct s at coef[s] + j*n (coefficient form, < q_j)
     const u64 *ntt[MAXS];    // the same digits in NTT form (inner-product diagonal)
+    const u64 *key[MAXS];    // switching key of ct s (adjacent cts usually share one)
 };
 
 // Key switching, step 2 (ModUp).  grid (S, l, l+1): digit j of ct s reduced into
@@ -208,7 +211,9 @@ struct RescaleArgs {
     const u64 *add[MAXS];         // nullable per s
     long long coef_pstride, base_pstride, out_pstride, add_pstride;
     int add_pmask;                // bit p set: add addend for output poly p
-    u32 add_g;                    // != 0: addend is read through the automorphism X -> X^g
+    u32 add_g[MAXS];              // != 0: addend of ct s is read through the automorphism X -> X^g
+    const u64 *acc[MAXS];         // nullable: second addend for both output polys (rotate-and-add)
+    long long acc_pstride;
     int src_id;                   // modulus id of the dropped prime
     u64 fac[MAXQ], fac_sh[MAXQ];
 };
@@ -237,18 +242,24 @@ __global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
         const int x = tid + e * C::TH;
         y[e] = shoup(subm(base[x], sm[C::pad(x)], M.q), f, fsh, M.q);
     }
-    if (add && a.add_g) {
+    const u32 add_g = a.add_g[s];
+    if (add && add_g) {
         __syncthreads();
         for (int x = tid; x < C::N; x += C::TH) sm[C::pad(x)] = add[x];
         __syncthreads();
 #pragma unroll
         for (int e = 0; e < C::E; e++) {
             const int x = tid + e * C::TH;
-            y[e] = addm(y[e], sm[C::pad(galois_perm(x, a.add_g, LOGN))], M.q);
+            y[e] = addm(y[e], sm[C::pad(galois_perm(x, add_g, LOGN))], M.q);
         }
     } else if (add) {
 #pragma unroll
         for (int e = 0; e < C::E; e++) y[e] = addm(y[e], add[tid + e * C::TH], M.q);
+    }
+    if (a.acc[s]) {
+        const u64 *acc = a.acc[s] + p * a.acc_pstride + i * n;
+#pragma unroll
+        for (int e = 0; e < C::E; e++) y[e] = addm(y[e], acc[tid + e * C::TH], M.q);
     }
 #pragma unroll
     for (int e = 0; e < C::E; e++) out[tid + e * C::TH] = y[e];
@@ -265,9 +276,11 @@ __global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
 // reused 4 times; products accumulate in 128 bits and are Montgomery-reduced
 // once per output (sum of l products < l q^2 < q 2^64 for l q < 2^64).
 #define KS_GROUP 4
-__global__ void k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, const u64 *__restrict__ key,
-                           u64 *__restrict__ Acc, int S, int l, int L, int logn, int special_id,
-                           const ModInfo *__restrict__ mods) {
+template <int LL>
+__global__ void __launch_bounds__(256) k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, u64 *__restrict__ Acc,
+                                                  int S, int L, int logn, int special_id,
+                                                  const ModInfo *__restrict__ mods) {
+    constexpr int l = LL;
     const long long n = 1ll << logn;
     const int groups = (S + KS_GROUP - 1) / KS_GROUP;
     GRID_STRIDE(idx, (long long)groups * (l + 1) * n) {
@@ -278,21 +291,33 @@ __global__ void k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, const u64 *
         const int kp = i == l ? L : i;
         const ModInfo &M = mods[i == l ? special_id : i];
         const u64 q = M.q, qi = M.qinv;
-        u64 kb[MAXQ], ka[MAXQ];
-        for (int j = 0; j < l; j++) {
-            kb[j] = __ldg(key + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
-            ka[j] = __ldg(key + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
-        }
+        u64 kb[l], ka[l];
+        const int sc = S - s0 < KS_GROUP ? S - s0 : KS_GROUP;
+        const u64 *cur = dt.key[s0];
 #pragma unroll
-        for (int u = 0; u < KS_GROUP; u++) {
+        for (int j = 0; j < l; j++) {
+            kb[j] = __ldg(cur + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
+            ka[j] = __ldg(cur + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
+        }
+        for (int u = 0; u < sc; u++) {
             const int s = s0 + u;
-            if (s >= S) break;
+            if (dt.key[s] != cur) {                   // a key boundary inside the group (multi-step batches)
+                cur = dt.key[s];
+#pragma unroll
+                for (int j = 0; j < l; j++) {
+                    kb[j] = __ldg(cur + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
+                    ka[j] = __ldg(cur + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
+                }
+            }
+            u64 e[l];
+#pragma unroll
+            for (int j = 0; j < l; j++)
+                e[j] = i == j ? dt.ntt[s][(long long)j * n + x] : Ext[((((long long)s * l + j) * (l + 1)) + i) * n + x];
             u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+#pragma unroll
             for (int j = 0; j < l; j++) {
-                const u64 e = i == j ? dt.ntt[s][(long long)j * n + x]
-                                     : Ext[((((long long)s * l + j) * (l + 1)) + i) * n + x];
-                mac128(h0, l0, e, kb[j]);
-                mac128(h1, l1, e, ka[j]);
+                mac128(h0, l0, e[j], kb[j]);
+                mac128(h1, l1, e[j], ka[j]);
             }
             Acc[(((long long)s * 2 + 0) * (l + 1) + i) * n + x] = mont_reduce(h0, l0, q, qi);
             Acc[(((long long)s * 2 + 1) * (l + 1) + i) * n + x] = mont_reduce(h1, l1, q, qi);

@@ -33,6 +33,7 @@ from .packing import (
     KernelSpec,
     _add_many,
     _mul_plain_many,
+    _rotate_multi,
     combine_to_dense,
     h_grouping,
     source_slots,
@@ -160,9 +161,13 @@ def _dense_assemble(x, w, kernel, ctx, blocks):
             dots = dots + (ctx.counters - before)
             before = ctx.counters.copy()
             masked = _mask_slot0_many(ctx, outs)
-            for i, ct in enumerate(masked):
-                pos = s0 + i - b0
-                acc = ct if acc is None else ctx.add_cc(acc, ctx.rotate(ct, (n - pos) % n))
+            first = 1 if acc is None else 0
+            if acc is None:
+                acc = masked[0]
+            moved = _rotate_multi(ctx, masked[first:], [(n - (s0 + i - b0)) % n
+                                                       for i in range(first, len(masked))])
+            for m in moved:
+                acc = ctx.add_cc(acc, m)
             asm = asm + (ctx.counters - before)
             s0 = s1
         results.append(acc)

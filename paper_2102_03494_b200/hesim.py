@@ -485,6 +485,33 @@ class HeContext:
                 outs[i] = self._wrap(h, cts[i].depth, cts[i].assembly_depth)
         return outs
 
+    def rotate_multi(self, cts, ks):
+        """rotate(cts[i], ks[i]) for every i: same counters and results, one
+        batched launch sequence (each ciphertext with its own key)."""
+        cts, ks = list(cts), [int(k) for k in ks]
+        n = self.params.n_slots
+        for k in ks:
+            if not 0 <= k < n:
+                raise ValueError(f"rotation amount must be in [0, {n}), got {k}")
+        outs = list(cts)
+        live = [i for i, k in enumerate(ks) if k != 0]
+        self.elided_rotations += len(cts) - len(live)
+        self.counters.rot += len(live)
+        if not live:
+            return outs
+        if not cts[live[0]].tracked:
+            for i in live:
+                outs[i] = SlotCiphertext(None, cts[i].depth, cts[i].params, cts[i].assembly_depth)
+            return outs
+        groups: dict[int, list[int]] = {}
+        for i in live:
+            groups.setdefault(cts[i].handle.level, []).append(i)
+        for idx in groups.values():
+            res = self.evaluator.rotate_multi([cts[i].handle for i in idx], [ks[i] for i in idx])
+            for i, h in zip(idx, res):
+                outs[i] = self._wrap(h, cts[i].depth, cts[i].assembly_depth)
+        return outs
+
     def add_cc_many(self, a, b):
         a, b = list(a), list(b)
         self.counters.add_cc += len(a)
@@ -510,8 +537,25 @@ class HeContext:
         rounds = (m - 1).bit_length()
         acc = cts
         for h in reversed(range(rounds)):
-            acc = self.add_cc_many(acc, self.rotate_many(acc, 1 << h))
+            acc = self._rotate_add_many(acc, 1 << h)
         return acc
+
+    def _rotate_add_many(self, cts, k: int):
+        """acc + rotate(acc, k) for every acc: one rotation and one addition each
+        (counted as such), fused on the device."""
+        self.counters.rot += len(cts)
+        self.counters.add_cc += len(cts)
+        if not cts[0].tracked:
+            return [SlotCiphertext(None, c.depth, c.params, c.assembly_depth) for c in cts]
+        groups: dict[int, list[int]] = {}
+        for i, c in enumerate(cts):
+            groups.setdefault(c.handle.level, []).append(i)
+        outs = [None] * len(cts)
+        for idx in groups.values():
+            res = self.evaluator.rotate_add_many([cts[i].handle for i in idx], k)
+            for i, h in zip(idx, res):
+                outs[i] = self._wrap(h, cts[i].depth, cts[i].assembly_depth)
+        return outs
 
 
 def merge_contexts(target: HeContext, *others: HeContext) -> HeContext:

@@ -204,6 +204,20 @@ class Evaluator:
                       handle_array([o.ptr for o in outs]), len(cts), int(k))
         return outs
 
+    def rotate_add_many(self, cts, k: int) -> list[Ciphertext]:
+        """out[i] = cts[i] + rotate(cts[i], k), fused."""
+        outs = [self.new_ct(c.rows, c.level) for c in cts]
+        self.lib.call("fhe_rotate_add_many", self.ctx, handle_array([c.ptr for c in cts]),
+                      handle_array([o.ptr for o in outs]), len(cts), int(k))
+        return outs
+
+    def rotate_multi(self, cts, ks) -> list[Ciphertext]:
+        outs = [self.new_ct(c.rows, c.level) for c in cts]
+        arr = (ctypes.c_uint32 * len(ks))(*[int(k) for k in ks])
+        self.lib.call("fhe_rotate_multi", self.ctx, handle_array([c.ptr for c in cts]),
+                      handle_array([o.ptr for o in outs]), arr, len(cts))
+        return outs
+
     def mul_plain_many(self, cts, pts) -> list[Ciphertext]:
         outs = [self.new_ct(c.rows, c.level) for c in cts]
         self.lib.call("fhe_mul_plain_many", self.ctx, handle_array([c.ptr for c in cts]),

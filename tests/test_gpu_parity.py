@@ -106,3 +106,17 @@ def test_chain_noise_and_decrypt(golden_lib, cuda_lib):
         cg, cc = gd.square(cg), gp.square(cc)
     assert np.array_equal(gd.read(cg), gp.read(cc))
     assert np.array_equal(gd.decrypt(cg), gp.decrypt(cc))
+
+
+def test_rotate_multi_matches_single(golden_lib, cuda_lib):
+    gd, gp, P = _pair(CASES[3], golden_lib, cuda_lib)
+    rng = np.random.default_rng(6)
+    cts = [gp.encrypt(_rand_slots(P, 1 + i % 3, rng)) for i in range(6)]
+    ks = [1, 4095, 3, 3, 8191, 77]
+    multi = gp.rotate_multi(cts, ks)
+    for c, k, m in zip(cts, ks, multi):
+        assert np.array_equal(gp.read(gp.rotate(c, k)), gp.read(m))
+    # and the golden model agrees word for word
+    cg = gd.new_ct(cts[1].rows)
+    gd.write(cg, gp.read(cts[1]))
+    assert np.array_equal(gd.read(gd.rotate(cg, 4095)), gp.read(multi[1]))
