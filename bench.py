@@ -365,30 +365,55 @@ def rotation_modmuls_L(n, l):
 
 
 def run_inference(args, rank, world, local_rank, images_total=None, steps=None, warmup=None):
+    """configs[2]: `images_total` images sharded contiguously over ranks, each
+    rank's shard evaluated in rounds of `chunk` images.  value: evaluation of
+    resident encrypted inputs (CUDA events, max over ranks).  e2e: rank 0 holds
+    the host images, encrypts and scatters them (NCCL), every rank evaluates,
+    rank 0 gathers the encrypted logits and decrypts them to host."""
     import torch
     from paper_2102_03494_b200.abi import cuda_library
     from paper_2102_03494_b200.hesim import HeContext
     from paper_2102_03494_b200.runner import pack_input, run_encrypted
+    from paper_2102_03494_b200.shard import gather_logits, scatter_packed, shard_range
 
     torch.cuda.set_device(local_rank)
+    device = f"cuda:{local_rank}"
     lib = cuda_library()
     images_total = images_total or args.images
     steps = steps if steps is not None else args.steps
     warmup = warmup if warmup is not None else args.warmup
-    per_rank = images_total // world
+    lo, hi = shard_range(images_total, rank, world)
+    per_rank = hi - lo
     chunk = min(args.chunk, per_rank)
-    net, plan, ws, xs, rp = cfg0_setup(per_rank, seed=CFG1["seed"], offset=rank * per_rank)
+    rounds = -(-per_rank // chunk)
+    net, plan, ws, xs_all, rp = cfg0_setup(images_total, seed=CFG1["seed"])
     ctx = HeContext(net.scheme, batch=chunk, lib=lib)
     ev = ctx.evaluator
     stream_ptr = ctypes.c_void_p()
     lib.call("fhe_ctx_stream", ev.ctx, ctypes.byref(stream_ptr))
     stream = torch.cuda.ExternalStream(stream_ptr.value, device=local_rank)
-    chunks = [xs[i:i + chunk] for i in range(0, per_rank, chunk)]
 
-    def evaluate(packed_list):
-        return [run_encrypted(net, plan, ws, None, ctx=ctx, packed=p, decrypt=False) for p in packed_list]
+    def round_images(k):
+        """every rank's k-th chunk, concatenated in rank order (rank 0's view)."""
+        parts = []
+        for r in range(world):
+            a, b = shard_range(images_total, r, world)
+            sub = xs_all[a:b][k * chunk:(k + 1) * chunk]
+            if len(sub) < chunk:                               # ragged tail: pad with zero images
+                sub = np.concatenate([sub, np.zeros((chunk - len(sub),) + sub.shape[1:], dtype=sub.dtype)])
+            parts.append(sub)
+        return np.concatenate(parts)
 
-    packed = [pack_input(net, plan, c, ctx) for c in chunks]
+    def scatter_round(k):
+        if world == 1:
+            return pack_input(net, plan, round_images(k), ctx)
+        return scatter_packed(net, plan, ctx, round_images(k) if rank == 0 else None, rank, world, device)
+
+    packed = [scatter_round(k) for k in range(rounds)]
+
+    def evaluate(ps):
+        return [run_encrypted(net, plan, ws, None, ctx=ctx, packed=p, decrypt=False) for p in ps]
+
     for _ in range(max(1, warmup)):
         evaluate(packed[:1])
     ev.sync()
@@ -410,18 +435,23 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt1))
     rots = ctx.counters.rot - rot0
     if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local_rank}")
+        t = torch.tensor([ms], device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    # e2e: host images -> encrypt -> evaluate -> decrypt logits to host
+    # e2e: host images on rank 0 -> encrypt + scatter -> evaluate -> gather + decrypt
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
-    logits = [run_encrypted(net, plan, ws, c, ctx=ctx).logits for c in chunks]
+    first_logits = None
+    for k in range(rounds):
+        res = run_encrypted(net, plan, ws, None, ctx=ctx, packed=scatter_round(k), decrypt=False)
+        lg = gather_logits(ctx, res.value, rank, world, device) if world > 1 else _decrypt_logits(res, ctx)
+        if first_logits is None:
+            first_logits = lg
     ev.sync()
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], device=f"cuda:{local_rank}")
+        t = torch.tensor([e2e_s], device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     # per-kernel breakdown of one chunk (single-stream, isolated kernel times)
@@ -434,20 +464,27 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     # physical ciphertext rotations: logical rotations x CRT primes x row pairs
     phys_rot = rots * rp.T * ctx.rows
     mm = phys_rot * rotation_modmuls(rp.n, rp.L)
+    in_bytes = int(np.prod(xs_all.shape[1:]) * 8 * images_total)
     return {
         "images_per_s": images_total * steps / (ms * 1e-3),
         "ms_per_step": ms / steps,
         "e2e_images_per_s": images_total / e2e_s,
-        "per_rank_images": per_rank, "chunk": chunk, "chunks": len(chunks),
+        "per_rank_images": per_rank, "chunk": chunk, "rounds": rounds,
         "crt_primes": len(rp.t), "t_bits": round(math.log2(rp.t[0]), 2), "L": rp.L,
-        "log_qp": round(rp.log_qp, 1), "logical_rotations_per_chunk": rots // max(1, steps * len(chunks)),
+        "log_qp": round(rp.log_qp, 1), "logical_rotations_per_chunk": rots // max(1, steps * rounds),
         "physical_rotations_per_s": world * phys_rot / (ms * 1e-3),
         "rotation_modmul_per_s_per_gpu": mm / (ms * 1e-3),
         "gpu_launches": int(cnt1.value - cnt0.value),
-        "h2d_bytes_per_step": int(xs.size * 8 * world), "d2h_bytes_per_step": int(10 * images_total * 8 * rp.T),
-        "clocks": clk.summary(), "logits_sample": [str(int(v)) for v in np.asarray(logits[0])[0][:3]],
+        "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": int(10 * images_total * 8 * rp.T),
+        "clocks": clk.summary(),
+        "logits_sample": [str(int(v)) for v in np.asarray(first_logits)[0][:3]] if first_logits is not None else None,
         "kernel_ms_one_chunk": breakdown,
     }
+
+
+def _decrypt_logits(res, ctx):
+    from paper_2102_03494_b200.runner import _logits
+    return np.atleast_2d(_logits(res.value, ctx))
 
 
 def cpu_baseline_inference(images: int = 1):

@@ -106,6 +106,10 @@ uint32_t fhe_ct_rows(const fhe_ct *ct);
 /* raw NTT-domain words, [T*R][2][level][n] */
 int fhe_ct_read(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *words);
 int fhe_ct_write(fhe_ctx *ctx, fhe_ct *ct, const uint64_t *words);
+/* the same words to/from caller-owned DEVICE memory (e.g. a torch CUDA tensor used as
+ * an NCCL send/recv buffer); the golden model treats the pointers as host memory */
+int fhe_ct_to_device(fhe_ctx *ctx, const fhe_ct *ct, void *dst);
+int fhe_ct_from_device(fhe_ctx *ctx, fhe_ct *ct, const void *src);
 /* transparent encryption of zero: (0, 0) */
 int fhe_ct_zero(fhe_ctx *ctx, fhe_ct *ct);
 

@@ -615,6 +615,8 @@ static u64 *poly(const fhe_ct *ct, u32 idx, u32 p, u32 i) {
 
 int fhe_ct_read(fhe_ctx *c, const fhe_ct *ct, uint64_t *w) { (void)c; memcpy(w, ct->data, ct_words(ct) * 8); return 0; }
 int fhe_ct_write(fhe_ctx *c, fhe_ct *ct, const uint64_t *w) { (void)c; memcpy(ct->data, w, ct_words(ct) * 8); return 0; }
+int fhe_ct_to_device(fhe_ctx *c, const fhe_ct *ct, void *dst) { (void)c; memcpy(dst, ct->data, ct_words(ct) * 8); return 0; }
+int fhe_ct_from_device(fhe_ctx *c, fhe_ct *ct, const void *src) { (void)c; memcpy(ct->data, src, ct_words(ct) * 8); return 0; }
 int fhe_ct_zero(fhe_ctx *c, fhe_ct *ct) { (void)c; memset(ct->data, 0, ct_words(ct) * 8); return 0; }
 
 int fhe_pt_create(fhe_ctx *c, fhe_pt **out) {

@@ -66,6 +66,8 @@ SIGNATURES = {
     "fhe_ct_read": (c_int, [c_void_p, c_void_p, _U64P]),
     "fhe_ct_write": (c_int, [c_void_p, c_void_p, _U64P]),
     "fhe_ct_zero": (c_int, [c_void_p, c_void_p]),
+    "fhe_ct_to_device": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "fhe_ct_from_device": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fhe_pt_create": (c_int, [c_void_p, POINTER(c_void_p)]),
     "fhe_pt_destroy": (None, [c_void_p]),
     "fhe_encode": (c_int, [c_void_p, _U64P, c_void_p]),

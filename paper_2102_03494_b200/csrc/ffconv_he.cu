@@ -796,6 +796,16 @@ extern "C" int fhe_ct_write(fhe_ctx *c, fhe_ct *ct, const uint64_t *w) {
     CU(cudaStreamSynchronize(c->st));
     return 0;
 }
+extern "C" int fhe_ct_to_device(fhe_ctx *c, const fhe_ct *ct, void *dst) {
+    CU(cudaMemcpyAsync(dst, ct->d, ct_words(ct) * 8, cudaMemcpyDeviceToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+extern "C" int fhe_ct_from_device(fhe_ctx *c, fhe_ct *ct, const void *src) {
+    CU(cudaMemcpyAsync(ct->d, src, ct_words(ct) * 8, cudaMemcpyDeviceToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
 extern "C" int fhe_ct_zero(fhe_ctx *c, fhe_ct *ct) {
     CU(cudaMemsetAsync(ct->d, 0, ct_words(ct) * 8, c->st));
     return 0;

@@ -104,6 +104,13 @@ class Evaluator:
             raise ValueError("word count does not match the ciphertext shape")
         self.lib.call("fhe_ct_write", self.ctx, ct.ptr, u64_ptr(w))
 
+    def export_words(self, ct: Ciphertext, ptr: int) -> None:
+        """Copy the ciphertext words into caller-owned device memory at `ptr`."""
+        self.lib.call("fhe_ct_to_device", self.ctx, ct.ptr, ctypes.c_void_p(ptr))
+
+    def import_words(self, ct: Ciphertext, ptr: int) -> None:
+        self.lib.call("fhe_ct_from_device", self.ctx, ct.ptr, ctypes.c_void_p(ptr))
+
     def encode(self, slots: np.ndarray) -> Plaintext:
         s = np.ascontiguousarray(slots, dtype=np.uint64)
         if s.shape != (self.T, self.n):
