@@ -328,7 +328,8 @@ def run_rotation(args, rank, world, local_rank):
             "kernel": dominant, "bound": "int", "achieved": d["modmul_per_s"] / 1e9,
             "peak": peak_modmul / 1e9, "unit": "Gmodmul/s", "frac": d["modmul_per_s"] / peak_modmul,
             "peak_source": "measured live: k_peak_modmul (chained 64-bit Shoup modmuls, all SMs)",
-            "hbm_gbs": d["gbs"], "hbm_peak_gbs": _hbm_peak(), "traffic": None,
+            "hbm_gbs": d["gbs"], "hbm_peak_gbs": _hbm_peak(), "traffic": _ncu_traffic(dominant),
+            "algorithmic": "per ciphertext: l*l NTTs of (n/2)log2(n) modmuls (k_modup); see DESIGN.md section 3",
         }
     return result
 
@@ -509,6 +510,27 @@ def _cpu_inference_task(args):
     net, plan, ws, xs, rp = cfg0_setup(1, seed=CFG1["seed"], offset=img_idx)
     run_encrypted(net, plan, ws, xs[0], ctx=SlotContext(Params(8192, ti)))
     return 1
+
+
+def _ncu_traffic(kernel: str):
+    """dram__bytes_read + dram__bytes_write per launch of `kernel` from the newest
+    committed `ncu --set full` summary in profiles/ (None if absent)."""
+    import glob
+    import re
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_prof_top.txt")), reverse=True):
+        text = open(path).read()
+        if kernel.split("(")[0] not in text.splitlines()[0]:
+            continue
+        vals = {}
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            m = re.search(name + r"\s+([0-9.]+)\s+(\w+)", text)
+            if m:
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(m.group(2), 1)
+                vals[name] = float(m.group(1)) * scale
+        if len(vals) == 2:
+            return {"bytes_per_launch": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+                    "source": os.path.relpath(path, ROOT)}
+    return None
 
 
 def _hbm_peak():

@@ -18,6 +18,7 @@
 
 #include "ffconv_he.h"
 #include "kernels.cuh"
+#include "ntt4.cuh"
 
 // =================================================================== errors
 static thread_local char g_err[512];
@@ -681,6 +682,36 @@ static int bench_variant(fhe_ctx *c, int inverse, u32 rows, u32 iters, const u64
     return 0;
 }
 
+template <int LOGN>
+static int bench_ntt4(fhe_ctx *c, int inverse, u32 rows, u32 iters, const u64 *in, u64 *out, float *ms) {
+    using C4 = Ntt4Cfg<LOGN>;
+    u64 *tmp;
+    CU(cudaMalloc((void **)&tmp, (size_t)rows * C4::N * 8));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const unsigned ga = rows * C4::CTAS_PER_ROW_A, gb = rows * C4::CTAS_PER_ROW_B;
+    for (u32 it = 0; it < iters + 2; it++) {
+        if (it == 2) cudaEventRecord(e0, c->st);
+        if (inverse) {
+            k4_inv_rows<LOGN><<<gb, C4::THB, 0, c->st>>>(in, tmp, c->d_mods, 0);
+            k4_inv_cols<LOGN><<<ga, C4::THA, 0, c->st>>>(tmp, out, c->d_mods, 0);
+        } else {
+            k4_fwd_cols<LOGN><<<ga, C4::THA, 0, c->st>>>(in, tmp, c->d_mods, 0);
+            k4_fwd_rows<LOGN><<<gb, C4::THB, 0, c->st>>>(tmp, out, c->d_mods, 0);
+        }
+    }
+    cudaEventRecord(e1, c->st);
+    CU(cudaEventSynchronize(e1));
+    CHECK_LAUNCH();
+    cudaEventElapsedTime(ms, e0, e1);
+    *ms /= iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(tmp);
+    return 0;
+}
+
 extern "C" int fhe_bench_ntt(fhe_ctx *c, int W, int inverse, uint32_t rows, uint32_t iters, float *ms,
                              uint32_t *mismatch) {
     if (c->logn != 14) return fail(FHE_EINVAL, "bench_ntt is instantiated for n = 2^14 only");
@@ -700,6 +731,7 @@ extern "C" int fhe_bench_ntt(fhe_ctx *c, int W, int inverse, uint32_t rows, uint
             case 4: rc = bench_variant<14, 4>(c, inverse, rows, iters, in, out, ms); break;
             case 5: rc = bench_variant<14, 5>(c, inverse, rows, iters, in, out, ms); break;
             case 6: rc = bench_variant<14, 6>(c, inverse, rows, iters, in, out, ms); break;
+            case 100: rc = bench_ntt4<14>(c, inverse, rows, iters, in, out, ms); break;
             default: rc = fail(FHE_EINVAL, "W must be in {3,4,5,6}");
         }
     }
@@ -1007,12 +1039,22 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_modup", k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
                                         c->d_mods));
     CHECK_LAUNCH();
-    long long tot = (long long)((S + KS_GROUP - 1) / KS_GROUP) * (l + 1) * n;
+    // inner-product variant: (ciphertexts per thread, min CTAs per SM); env FHE_KS_VARIANT=0..3
+    static int ksv = -1;
+    if (ksv < 0) { const char *e = getenv("FHE_KS_VARIANT"); ksv = e ? atoi(e) : 2; }   // 2: measured best (4 cts/thread, 4 CTAs/SM)
+    const int G = (ksv == 1 || ksv == 3) ? 2 : 4;
+    long long tot = (long long)((S + G - 1) / G) * (l + 1) * n;
     {
         ProfScope ps_(c, "k_ks_inner");
         const unsigned nb = (unsigned)nblocks(tot);
-#define KS_CASE(LLV) case LLV: k_ks_inner<LLV><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, (int)c->logn, \
-                                                                       c->special_id, c->d_mods); break;
+#define KS_LAUNCH(LLV, GV, MB) k_ks_inner<LLV, GV, MB><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, \
+                                                        (int)c->logn, c->special_id, c->d_mods)
+#define KS_CASE(LLV) case LLV:                                        \
+        if (ksv == 1) KS_LAUNCH(LLV, 2, 1);                           \
+        else if (ksv == 2) KS_LAUNCH(LLV, 4, 4);                      \
+        else if (ksv == 3) KS_LAUNCH(LLV, 2, 4);                      \
+        else KS_LAUNCH(LLV, 4, 1);                                    \
+        break;
         switch (l) {
             KS_CASE(1) KS_CASE(2) KS_CASE(3) KS_CASE(4) KS_CASE(5) KS_CASE(6) KS_CASE(7) KS_CASE(8)
             KS_CASE(9) KS_CASE(10) KS_CASE(11) KS_CASE(12) KS_CASE(13) KS_CASE(14) KS_CASE(15) KS_CASE(16)
@@ -1020,6 +1062,7 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
             default: return fail(FHE_EINVAL, "level %u unsupported by k_ks_inner", l);
         }
 #undef KS_CASE
+#undef KS_LAUNCH
     }
     CHECK_LAUNCH();
     // ModDown: INTT of the special limb of both accumulators

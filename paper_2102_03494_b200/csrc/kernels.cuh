@@ -275,11 +275,10 @@ __global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
 // (group of 4 cts, prime i, coefficient x): the 2l key words are loaded once and
 // reused 4 times; products accumulate in 128 bits and are Montgomery-reduced
 // once per output (sum of l products < l q^2 < q 2^64 for l q < 2^64).
-#define KS_GROUP 4
-template <int LL>
-__global__ void __launch_bounds__(256) k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, u64 *__restrict__ Acc,
-                                                  int S, int L, int logn, int special_id,
-                                                  const ModInfo *__restrict__ mods) {
+template <int LL, int KS_GROUP, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, u64 *__restrict__ Acc,
+                                                     int S, int L, int logn, int special_id,
+                                                     const ModInfo *__restrict__ mods) {
     constexpr int l = LL;
     const long long n = 1ll << logn;
     const int groups = (S + KS_GROUP - 1) / KS_GROUP;

@@ -154,3 +154,4 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
 #pragma unroll
     for (int e = 0; e < E; e++) v[e] = shoup(v[e], M.ninv, M.ninv_sh, q);
 }
+
