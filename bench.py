@@ -361,6 +361,88 @@ def cfg0_setup(images: int, seed: int, offset: int = 0):
     return net, plan, ws, xs, rp
 
 
+ABLATION = [
+    # (name, first layer spec) -- the configs[4] variants: unfactorized 5x5 conv vs FFConv ranks,
+    # each under DensePack and ConvPack, followed by square, fc100, square, fc10
+    ("conv-dense", dict(kind="conv", d=5, stride=2, out_channels=5, packing_hint="dense")),
+    ("conv-cp", dict(kind="conv", d=5, stride=2, out_channels=5, packing_hint="conv")),
+    ("ffconv-r1-dp", dict(kind="ffconv", d=5, stride=2, out_channels=5, rank=1, packing_hint="dp-hi2c-cp")),
+    ("ffconv-r2-dp", dict(kind="ffconv", d=5, stride=2, out_channels=5, rank=2, packing_hint="dp-hi2c-cp")),
+    ("ffconv-r4-dp", dict(kind="ffconv", d=5, stride=2, out_channels=5, rank=4, packing_hint="dp-hi2c-cp")),
+    ("ffconv-r1-cp", dict(kind="ffconv", d=5, stride=2, out_channels=5, rank=1, packing_hint="cp-hi2c-cp")),
+    ("ffconv-r2-cp", dict(kind="ffconv", d=5, stride=2, out_channels=5, rank=2, packing_hint="cp-hi2c-cp")),
+    ("ffconv-r4-cp", dict(kind="ffconv", d=5, stride=2, out_channels=5, rank=4, packing_hint="cp-hi2c-cp")),
+]
+
+
+def ablation_setup(first, images, seed, offset=0):
+    from paper_2102_03494_b200.hesim import SchemeParams
+    from paper_2102_03494_b200.netspec import LayerSpec, NetworkSpec, synthetic_weights
+    from paper_2102_03494_b200.packing import TensorShape
+    from paper_2102_03494_b200.planner import build_plan
+    from paper_2102_03494_b200.runner import inference_params, scheme_for
+    layers = (LayerSpec(**first), LayerSpec("square"), LayerSpec("fc", out_channels=100), LayerSpec("square"),
+              LayerSpec("fc", out_channels=10))
+    shape = TensorShape(29, 29, 1)
+    prov = NetworkSpec(SchemeParams(n_slots=8192, t=(1 << 61) - 1), shape, layers)
+    ws = synthetic_weights(prov, np.random.default_rng(seed), sigma=0.1)
+    rp = inference_params(prov, build_plan(prov, "explicit"), ws, input_bound=255)
+    net = NetworkSpec(scheme_for(rp), shape, layers)
+    rng = np.random.default_rng(seed + 1)
+    pix = np.round(rng.random(size=(offset + images, 1, 28, 28)) * 255).astype(np.int64)[offset:]
+    xs = np.zeros((images, 1, 29, 29), dtype=np.int64)
+    xs[:, :, :28, :28] = pix
+    return net, build_plan(net, "explicit"), ws, xs, rp
+
+
+def run_ablation(args, rank, world, local_rank):
+    """configs[4]: rotation count and latency per variant (images sharded over ranks)."""
+    import torch
+    from paper_2102_03494_b200.abi import cuda_library
+    from paper_2102_03494_b200.hesim import HeContext
+    from paper_2102_03494_b200.runner import pack_input, run_encrypted
+    from paper_2102_03494_b200.shard import shard_range
+    torch.cuda.set_device(local_rank)
+    lib = cuda_library()
+    lo, hi = shard_range(args.images, rank, world)
+    per_rank = hi - lo
+    out = {}
+    for name, first in ABLATION:
+        net, plan, ws, xs, rp = ablation_setup(first, per_rank, seed=CFG1["seed"], offset=lo)
+        chunk = min(args.chunk, per_rank)
+        ctx = HeContext(net.scheme, batch=chunk, lib=lib)
+        chunks = [xs[i:i + chunk] for i in range(0, per_rank, chunk)]
+        if len(chunks[-1]) < chunk:
+            pad = np.zeros((chunk - len(chunks[-1]),) + xs.shape[1:], dtype=xs.dtype)
+            chunks[-1] = np.concatenate([chunks[-1], pad])
+        packed = [pack_input(net, plan, c, ctx) for c in chunks]
+        run_encrypted(net, plan, ws, None, ctx=ctx, packed=packed[0], decrypt=False)     # warm-up: keys, plaintexts
+        ctx.evaluator.sync()
+        if world > 1:
+            torch.distributed.barrier()
+        c0 = ctx.counters.copy()
+        t0 = time.perf_counter()
+        for p in packed:
+            res = run_encrypted(net, plan, ws, None, ctx=ctx, packed=p, decrypt=False)
+        ctx.evaluator.sync()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=f"cuda:{local_rank}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        d = ctx.counters - c0
+        per_chunk = len(packed)
+        out[name] = {"rotations_per_image": d.rot // per_chunk, "mul_pc_per_image": d.mul_pc // per_chunk,
+                     "add_cc_per_image": d.add_cc // per_chunk, "assembly_masks_per_image": d.assembly_mul_pc // per_chunk,
+                     "crt_primes": len(rp.t), "L": rp.L, "images_per_s": args.images / el,
+                     "latency_ms_per_batch": 1e3 * el / per_chunk, "batch": chunk,
+                     "depth": res.depth, "assembly_depth": res.assembly_depth}
+        del ctx, packed, res
+    return out
+
+
+
+
 def rotation_modmuls_L(n, l):
     return rotation_modmuls(n, l)
 
@@ -596,7 +678,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["rotation", "inference"], default="rotation")
+    ap.add_argument("--workload", choices=["rotation", "inference", "ablation"], default="rotation")
     ap.add_argument("--images", type=int, default=256, help="inference: images per step (whole job)")
     ap.add_argument("--chunk", type=int, default=64, help="inference: images per ciphertext batch")
     ap.add_argument("--no-inference", action="store_true", help="rotation workload: skip the inference sample")
@@ -613,6 +695,21 @@ def main():
         import torch
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    if args.workload == "ablation":
+        abl = run_ablation(args, rank, world, local_rank)
+        if rank == 0:
+            best = max(abl.values(), key=lambda v: v["images_per_s"])
+            print(json.dumps({
+                "metric": "encrypted-image inferences/s per packing/rank variant (configs[4] ablation)",
+                "value": best["images_per_s"], "unit": "images/s (best variant)", "n_gpus": world,
+                "steps": 1, "warmup": 1, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "u64", "data": "synthetic (seeded images)",
+                "config": {"workload": f"configs[4]: {args.images} images, chunks of {args.chunk}"},
+                "variants": abl}), flush=True)
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+        return
     if args.workload == "inference":
         inf = run_inference(args, rank, world, local_rank)
         res = {
