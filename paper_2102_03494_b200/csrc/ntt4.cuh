@@ -301,3 +301,4 @@ __global__ void __launch_bounds__(Ntt4Cfg<LOGN>::THA) k4_inv_cols(const u64 *tmp
     for (int e = 0; e < 8; e++)
         dst[(long long)lidx(tau, e, fl) << LB] = shoup(v[e], M.ninv, M.ninv_sh, M.q);
 }
+

@@ -4,13 +4,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2102_03494_b200.params import make_params
 from paper_2102_03494_b200.rlwe import Evaluator
 
-P = make_params(8192, [65537], levels=2, q_bits=59, p_bits=60, aux=False)
+P = make_params(8192, [65537], levels=2, q_bits=int(os.environ.get('QBITS', 59)), p_bits=int(os.environ.get('QBITS', 59)) + 1, aux=False)
 ev = Evaluator(P)
 peak = ctypes.c_double()
 ev.lib.call("fhe_peak_modmul", ev.ctx, 20000, ctypes.byref(peak))
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 1184
 out = {"peak_gmodmul": peak.value / 1e9, "rows": rows}
-for inv, Ws in ((0, (4, 5, 100)), (1, (4, 5, 100))):
+WS = os.environ.get("WS")
+plan = ((0, tuple(int(w) for w in WS.split(","))),) if WS else ((0, (4, 5, 100)), (1, (4, 5, 100)))
+for inv, Ws in plan:
     for W in Ws:
         ms, bad = ctypes.c_float(), ctypes.c_uint32()
         ev.lib.call("fhe_bench_ntt", ev.ctx, W, inv, rows, 20, ctypes.byref(ms), ctypes.byref(bad))
