@@ -248,10 +248,21 @@ def cfg0(images=2, seed=20210205):
         json.dump(meta, fh, indent=1)
 
 
+
+def weight_file():
+    """A CPKW0001 file written by the reference (weights.py:102-124)."""
+    from cipherpack.weights import save_weights as ref_save
+    ws = WeightSet([WeightTensor(name="layer0.weight", values=np.arange(-12, 12).reshape(2, 3, 4), bits=8,
+                                 scale=0.125),
+                    WeightTensor(name="layer0.bias", values=np.array([7, -3]), bits=8, scale=1.0)])
+    ref_save(ws, os.path.join(HERE, "weights_ref.cpkw"))
+
+
 if __name__ == "__main__":
     with open(os.path.join(HERE, "hesim_sequences.json"), "w") as fh:
         json.dump(hesim_sequences(), fh)
     with open(os.path.join(HERE, "networks.json"), "w") as fh:
         json.dump(networks(), fh)
     cfg0()
+    weight_file()
     print("fixtures written to", HERE)
