@@ -447,7 +447,7 @@ def rotation_modmuls_L(n, l):
     return rotation_modmuls(n, l)
 
 
-def run_inference(args, rank, world, local_rank, images_total=None, steps=None, warmup=None):
+def run_inference(args, rank, world, local_rank, images_total=None, steps=None, warmup=None, schedule=None):
     """configs[2]: `images_total` images sharded contiguously over ranks, each
     rank's shard evaluated in rounds of `chunk` images.  value: evaluation of
     resident encrypted inputs (CUDA events, max over ranks).  e2e: rank 0 holds
@@ -470,7 +470,8 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     chunk = min(args.chunk, per_rank)
     rounds = -(-per_rank // chunk)
     net, plan, ws, xs_all, rp = cfg0_setup(images_total, seed=CFG1["seed"])
-    ctx = HeContext(net.scheme, batch=chunk, lib=lib)
+    schedule = schedule or args.schedule
+    ctx = HeContext(net.scheme, batch=chunk, lib=lib, schedule=schedule)
     ev = ctx.evaluator
     stream_ptr = ctypes.c_void_p()
     lib.call("fhe_ctx_stream", ev.ctx, ctypes.byref(stream_ptr))
@@ -549,6 +550,7 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     mm = phys_rot * rotation_modmuls(rp.n, rp.L)
     in_bytes = int(np.prod(xs_all.shape[1:]) * 8 * images_total)
     return {
+        "schedule": schedule,
         "images_per_s": images_total * steps / (ms * 1e-3),
         "ms_per_step": ms / steps,
         "e2e_images_per_s": images_total / e2e_s,
@@ -682,6 +684,8 @@ def main():
     ap.add_argument("--images", type=int, default=256, help="inference: images per step (whole job)")
     ap.add_argument("--chunk", type=int, default=64, help="inference: images per ciphertext batch")
     ap.add_argument("--no-inference", action="store_true", help="rotation workload: skip the inference sample")
+    ap.add_argument("--schedule", choices=["reference", "hoisted"], default="reference",
+                    help="inference: rotate-and-sum schedule (hoisted = top levels as a ct x pt GEMM)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -732,9 +736,15 @@ def main():
     res = run_rotation(args, rank, world, local_rank)
     if not args.no_inference:
         # secondary line item: configs[2]-shaped inference on a bounded sample per GPU
-        inf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=1, warmup=1)
+        inf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=1, warmup=1,
+                            schedule="reference")
         res["inference"] = inf
         res["rates"]["images_per_s"] = inf["images_per_s"]
+        hinf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=1, warmup=1,
+                             schedule="hoisted")
+        res["inference_hoisted"] = {k: hinf[k] for k in ("schedule", "images_per_s", "e2e_images_per_s",
+                                                         "logical_rotations_per_chunk", "kernel_ms_one_chunk")}
+        res["rates"]["images_per_s_hoisted"] = hinf["images_per_s"]
     if rank == 0 and world == 1:
         rate, sample = cpu_baseline_rotation(1, seconds=3.0)
         res["cpu_baseline"] = {"value": rate, "unit": "rotations/s", "cores": 1, "kind": "port",

@@ -144,6 +144,13 @@ int fhe_mod_switch(fhe_ctx *ctx, const fhe_ct *a, fhe_ct *out);
 /* slot-wise square with relinearization; out must not alias a */
 int fhe_square(fhe_ctx *ctx, const fhe_ct *a, fhe_ct *out);
 
+/* hoisted dot products: out[s] = sum_k R[k] * tau_{g[k]}(pt[s]) for s < S, where
+ * tau_g is the plaintext automorphism X -> X^g (a slot rotation, applied in the
+ * NTT domain) and every R[k] has the shape of out[s].  With R[k] = rotate(x, k_i)
+ * and g[k] = 5^k_i this equals sum_k rotate(x * pt[s], k_i) slot for slot: the top
+ * levels of S rotate-and-sum trees over one input, as a modular GEMM. */
+int fhe_hoisted_dot(fhe_ctx *ctx, fhe_ct *const *R, const uint32_t *g, uint32_t K, fhe_pt *const *pt,
+                    uint32_t S, fhe_ct *const *out);
 /* batched forms: m independent operations in one launch sequence */
 int fhe_rotate_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k);
 /* out[i] = a[i] + rotate(a[i], k): one rotate-and-sum level, the addition fused

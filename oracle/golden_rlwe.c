@@ -1035,6 +1035,33 @@ int fhe_square(fhe_ctx *c, const fhe_ct *a, fhe_ct *out) {
     return 0;
 }
 
+int fhe_hoisted_dot(fhe_ctx *c, fhe_ct *const *R, const uint32_t *g, uint32_t K, fhe_pt *const *pt,
+                    uint32_t S, fhe_ct *const *out) {
+    if (!K) return fail(FHE_EINVAL, "hoisted_dot: K must be >= 1");
+    u32 n = c->n, l = R[0]->level;
+    for (u32 k = 0; k < K; k++)
+        if (!same_shape(R[k], R[0]) || !(g[k] & 1)) return fail(FHE_EINVAL, "hoisted_dot: bad operand %u", k);
+    u64 *tp = (u64 *)malloc((size_t)n * 8);
+    for (u32 s = 0; s < S; s++) {
+        if (!same_shape(out[s], R[0])) { free(tp); return fail(FHE_ELEVEL, "hoisted_dot: output shape mismatch"); }
+        memset(out[s]->data, 0, ct_words(out[s]) * 8);
+        for (u32 k = 0; k < K; k++)
+            for (u32 ci = 0; ci < R[0]->count; ci++) {
+                u32 kt = ci / R[0]->R;
+                for (u32 i = 0; i < l; i++) {
+                    u64 q = c->P.q[i];
+                    automorph(c, pt[s]->ntt_q + ((size_t)kt * c->L + i) * n, tp, g[k]);
+                    for (u32 p = 0; p < 2; p++) {
+                        const u64 *x = poly(R[k], ci, p, i);
+                        u64 *z = poly(out[s], ci, p, i);
+                        for (u32 j = 0; j < n; j++) z[j] = addmod(z[j], mulmod(x[j], tp[j], q), q);
+                    }
+                }
+            }
+    }
+    free(tp);
+    return 0;
+}
 int fhe_rotate_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k) {
     for (u32 i = 0; i < m; i++) { int rc = fhe_rotate(c, a[i], k, out[i]); if (rc) return rc; }
     return 0;

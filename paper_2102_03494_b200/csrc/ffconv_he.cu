@@ -1223,6 +1223,33 @@ extern "C" int fhe_rotate_multi(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out
     return rotate_phys(c, in, o, l, g);
 }
 
+extern "C" int fhe_hoisted_dot(fhe_ctx *c, fhe_ct *const *R, const uint32_t *g, uint32_t K, fhe_pt *const *pt,
+                               uint32_t S, fhe_ct *const *out) {
+    if (K < 1 || K > HMAXK) return fail(FHE_EINVAL, "hoisted_dot: K must be in [1, %d]", HMAXK);
+    for (u32 k = 0; k < K; k++)
+        if (!same_shape(R[k], R[0]) || !(g[k] & 1) || g[k] >= 2 * c->n) return fail(FHE_EINVAL, "hoisted_dot: bad operand %u", k);
+    const u32 l = R[0]->level;
+    for (u32 s0 = 0; s0 < S; s0 += HTILE) {
+        const u32 St = std::min<u32>(HTILE, S - s0);
+        HoistArgs a;
+        memset(&a, 0, sizeof a);
+        for (u32 k = 0; k < K; k++) { a.R[k] = R[k]->d; a.g[k] = g[k]; }
+        for (u32 s = 0; s < St; s++) {
+            if (!same_shape(out[s0 + s], R[0])) return fail(FHE_ELEVEL, "hoisted_dot: output shape mismatch");
+            if (!pt[s0 + s]->encoded) return fail(FHE_EINVAL, "hoisted_dot: plaintext was never encoded");
+            a.pt[s] = pt[s0 + s]->ntt_m;
+            a.out[s] = out[s0 + s]->d;
+        }
+        a.K = (int)K; a.S = (int)St; a.Rr = (int)R[0]->R; a.l = (int)l; a.L = (int)c->L; a.logn = (int)c->logn;
+        dim3 grid((unsigned)(c->n / 32 > 0 ? c->n / 32 : 1), c->T * l, (St + 7) / 8);
+        if (c->n < 32) return fail(FHE_EINVAL, "hoisted_dot needs n >= 32");
+        ProfScope ps_(c, "k_hoisted_dot");
+        k_hoisted_dot<<<grid, 256, 0, c->st>>>(a, c->d_mods);
+        CHECK_LAUNCH();
+    }
+    return 0;
+}
+
 extern "C" int fhe_mul_plain_many(fhe_ctx *c, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m) {
     for (u32 i = 0; i < m; i++) TRY(fhe_mul_plain(c, a[i], pt[i], out[i]));
     return 0;

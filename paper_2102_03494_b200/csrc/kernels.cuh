@@ -696,3 +696,72 @@ __global__ void __launch_bounds__(NttCfg<LOGN, W>::TH) k_bench_inv(const u64 *in
 #pragma unroll
     for (int e = 0; e < C::E; e++) dst[(e << (LOGN - C::W)) | tid] = v[e];
 }
+
+// ------------------------------------------------------------ hoisted dot
+// out[s][c][i][j] = sum_k R[k][c][i][j] * tau_{g_k}(pt[s])[t][i][j]   (c = (t, r, poly))
+// CTA = 32 coefficients x 8 outputs (one warp per output); R tiles of 8 rotations x
+// 8 columns staged in shared memory; products accumulate in 128 bits and are
+// Montgomery-reduced once per 8 rotations (8 q^2 < q 2^64).  Plaintexts are in
+// Montgomery form, so the reduction returns canonical residues.
+#define HMAXK 64
+#define HTILE 64
+struct HoistArgs {
+    const u64 *R[HMAXK];
+    u32 g[HMAXK];
+    const u64 *pt[HTILE];
+    u64 *out[HTILE];
+    int K, S, Rr, l, L, logn;
+};
+
+__global__ void __launch_bounds__(256) k_hoisted_dot(HoistArgs a, const ModInfo *__restrict__ mods) {
+    __shared__ u64 sm[8 * 8 * 32];
+    const int jl = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const long long n = 1ll << a.logn;
+    const int t = blockIdx.y / a.l, i = blockIdx.y % a.l;
+    const long long jb = (long long)blockIdx.x * 32;
+    const long long j = jb + jl;
+    const int s = blockIdx.z * 8 + sl;
+    const ModInfo &M = mods[i];
+    const u64 q = M.q, qi = M.qinv;
+    const int C = 2 * a.Rr;
+    const u64 *pt = s < a.S ? a.pt[s] + ((long long)t * a.L + i) * n : nullptr;
+    for (int cb = 0; cb < C; cb += 8) {
+        u64 sum[8];
+#pragma unroll
+        for (int cc = 0; cc < 8; cc++) sum[cc] = 0;
+        for (int kc = 0; kc < a.K; kc += 8) {
+            __syncthreads();
+#pragma unroll
+            for (int w = 0; w < 8; w++) {
+                const int idx = w * 256 + threadIdx.x;
+                const int kk = idx >> 8, cc = (idx >> 5) & 7, jj = idx & 31;
+                const int k = kc + kk, c = cb + cc;
+                u64 val = 0;
+                if (k < a.K && c < C)
+                    val = a.R[k][((((long long)t * a.Rr + (c >> 1)) * 2 + (c & 1)) * a.l + i) * n + jb + jj];
+                sm[idx] = val;
+            }
+            __syncthreads();
+            if (pt) {
+                u64 hi[8], lo[8];
+#pragma unroll
+                for (int cc = 0; cc < 8; cc++) { hi[cc] = 0; lo[cc] = 0; }
+                const int kn = a.K - kc < 8 ? a.K - kc : 8;
+                for (int kk = 0; kk < kn; kk++) {
+                    const u64 P = __ldg(pt + galois_perm((u32)j, a.g[kc + kk], a.logn));
+#pragma unroll
+                    for (int cc = 0; cc < 8; cc++) mac128(hi[cc], lo[cc], sm[(kk * 8 + cc) * 32 + jl], P);
+                }
+#pragma unroll
+                for (int cc = 0; cc < 8; cc++) sum[cc] = addm(sum[cc], mont_reduce(hi[cc], lo[cc], q, qi), q);
+            }
+        }
+        if (pt) {
+#pragma unroll
+            for (int cc = 0; cc < 8; cc++) {
+                const int c = cb + cc;
+                if (c < C) a.out[s][((((long long)t * a.Rr + (c >> 1)) * 2 + (c & 1)) * a.l + i) * n + j] = sum[cc];
+            }
+        }
+    }
+}

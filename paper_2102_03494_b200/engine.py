@@ -118,7 +118,7 @@ def _group_size(ctx) -> int:
     return max(1, int(getattr(ctx, "group_size", 1 << 30)))
 
 
-def _dense_dots(x: DensePacked, w: WeightMatrix, kernel: KernelSpec, ctx, o: int, s0: int, s1: int):
+def _dense_dots(x: DensePacked, w: WeightMatrix, kernel: KernelSpec, ctx, o: int, s0: int, s1: int, hoist=None):
     """Dot products of outputs (o, s0..s1-1): scatter the filter column to each
     patch, multiply, rotate-and-sum over the occupied span; result in slot 0
     (engine.py:104-121)."""
@@ -128,8 +128,59 @@ def _dense_dots(x: DensePacked, w: WeightMatrix, kernel: KernelSpec, ctx, o: int
     col = w.entries[:, o]
     tracked = x.ct.tracked
     pvs = [_scatter_plain(ctx, idx[s], col, tracked) for s in range(s0, s1)]
-    prods = _mul_plain_many(ctx, [x.ct] * (s1 - s0), pvs)
-    return _rotate_and_sum_many(ctx, prods, x.occupied)
+    return _products_and_sums(ctx, x.ct, pvs, x.occupied, hoist)
+
+
+# cost of one ct x pt GEMM term relative to one key-switched rotation of the same
+# ciphertext (2 l n MACs vs (l^2 + 3l + 2) n-point NTTs): conservatively 1/64
+GEMM_TERM_COST = 1.0 / 64
+
+
+def hoist_depth(outputs: int, rounds: int, max_levels: int) -> int:
+    """Tree levels to hoist for `outputs` trees over one input: maximise the
+    rotations saved (outputs * h) minus the input rotations (2^h - 1) and the
+    extra GEMM terms (outputs * (2^h - 1) * GEMM_TERM_COST)."""
+    best, best_gain = 0, 0.0
+    for h in range(1, min(max_levels, rounds) + 1):
+        gain = outputs * h - (2 ** h - 1) - outputs * (2 ** h - 1) * GEMM_TERM_COST
+        if gain > best_gain:
+            best, best_gain = h, gain
+    return best
+
+
+class _Hoist:
+    """Rotations of one shared input by every subset sum of the top h steps of a
+    rotate-and-sum tree, computed once per layer and reused by all its outputs."""
+
+    def __init__(self, ctx, ct, m: int, outputs: int):
+        r = (m - 1).bit_length()
+        self.h = hoist_depth(outputs, r, int(getattr(ctx, "hoist_levels", 7)))
+        self.tail = [1 << i for i in reversed(range(r - self.h))]      # remaining steps, largest first
+        ks = [0]
+        for i in range(self.h):
+            step = 1 << (r - 1 - i)
+            ks = ks + [k + step for k in ks]
+        self.ks = ks
+        rot = _rotate_multi(ctx, [ct] * (len(ks) - 1), ks[1:]) if len(ks) > 1 else []
+        self.rotated = [ct] + list(rot)
+
+
+def _hoisted(ctx) -> bool:
+    return getattr(ctx, "schedule", "reference") == "hoisted" and hasattr(ctx, "hoisted_dot")
+
+
+def _products_and_sums(ctx, ct, pvs, m: int, hoist):
+    """rotate_and_sum(ct * pv, m) for every pv.  Reference schedule: one product
+    and ceil(log2 m) rotate-add levels each.  Hoisted schedule: the top h levels of
+    every tree as one ct x pt GEMM over the shared input's rotations."""
+    if hoist is None:
+        return _rotate_and_sum_many(ctx, _mul_plain_many(ctx, [ct] * len(pvs), pvs), m)
+    if hoist.h == 0:
+        return _rotate_and_sum_many(ctx, _mul_plain_many(ctx, [ct] * len(pvs), pvs), m)
+    outs = ctx.hoisted_dot(hoist.rotated, hoist.ks, pvs)
+    for step in hoist.tail:
+        outs = ctx._rotate_add_many(outs, step)
+    return outs
 
 
 def _mask_slot0_many(ctx, cts):
@@ -148,6 +199,7 @@ def _dense_assemble(x, w, kernel, ctx, blocks):
     n = ctx.params.n_slots
     rows = len(source_slots(x.shape, kernel))       # outputs per channel
     g = _group_size(ctx)
+    hoist = None
     dots, asm = OpCounters(), OpCounters()
     results = []
     for b0, b1 in blocks:
@@ -157,7 +209,9 @@ def _dense_assemble(x, w, kernel, ctx, blocks):
             o = s0 // rows
             s1 = min(b1, (o + 1) * rows, s0 + g)
             before = ctx.counters.copy()
-            outs = _dense_dots(x, w, kernel, ctx, o, s0 - o * rows, s1 - o * rows)
+            if hoist is None and _hoisted(ctx) and x.ct.tracked:
+                hoist = _Hoist(ctx, x.ct, x.occupied, w.out_channels * rows)
+            outs = _dense_dots(x, w, kernel, ctx, o, s0 - o * rows, s1 - o * rows, hoist)
             dots = dots + (ctx.counters - before)
             before = ctx.counters.copy()
             masked = _mask_slot0_many(ctx, outs)
@@ -261,11 +315,14 @@ def fc_dense(x: DensePacked, w: WeightMatrix, bias: BiasVector | None, ctx, mask
     g = _group_size(ctx)
     rows, masks = OpCounters(), OpCounters()
     outs = []
+    hoist = None
     for o0 in range(0, w.out_channels, g):
         o1 = min(w.out_channels, o0 + g)
         before = ctx.counters.copy()
+        if hoist is None and _hoisted(ctx) and tracked:
+            hoist = _Hoist(ctx, x.ct, m, w.out_channels)
         pvs = [_prefix_values(ctx, w.entries[:, o], tracked) for o in range(o0, o1)]
-        red = _rotate_and_sum_many(ctx, _mul_plain_many(ctx, [x.ct] * (o1 - o0), pvs), m)
+        red = _products_and_sums(ctx, x.ct, pvs, m, hoist)
         if bias is not None:
             red = [ctx.add_plain(r, _scatter_plain(ctx, [0], [int(bias.entries[o])], tracked))
                    for o, r in zip(range(o0, o1), red)]

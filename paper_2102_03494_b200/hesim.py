@@ -201,7 +201,8 @@ class HeContext:
     """
 
     def __init__(self, params: SchemeParams, *, batch: int = 1, lib=None, levels: int | None = None,
-                 q_bits: int | None = None, debug_checks: bool = False, pt_cache: bool = True):
+                 q_bits: int | None = None, debug_checks: bool = False, pt_cache: bool = True,
+                 schedule: str = "reference", hoist_levels: int = 7):
         if batch < 1:
             raise ValueError("batch must be >= 1")
         self.params = params
@@ -215,6 +216,13 @@ class HeContext:
         self._q_bits = q_bits
         self._ev = None
         self._pt_cache = {} if pt_cache else None
+        if schedule not in ("reference", "hoisted"):
+            raise ValueError("schedule must be 'reference' or 'hoisted'")
+        # "hoisted": the top hoist_levels levels of rotate-and-sum trees that share
+        # one input are evaluated as rotations of the input + a ct x pt GEMM
+        # (engine._dense_dots / fc_dense); decrypted slots are identical, op counts differ
+        self.schedule = schedule
+        self.hoist_levels = hoist_levels
 
     # ------------------------------------------------------------------ device
     @property
@@ -484,6 +492,32 @@ class HeContext:
             for i, h in zip(idx, res):
                 outs[i] = self._wrap(h, cts[i].depth, cts[i].assembly_depth)
         return outs
+
+    def hoisted_dot(self, rotated, ks, pvs):
+        """out[s] = sum_k rotated[k] * rot_{ks[k]}(pvs[s]) where rotated[k] =
+        rotate(x, ks[k]) (ks[0] = 0): equal, slot for slot, to sum_k rotate(x * pv_s, ks[k]).
+        Counts len(ks) plaintext products and len(ks) - 1 additions per output."""
+        rotated, ks, pvs = list(rotated), [int(k) for k in ks], list(pvs)
+        S, K = len(pvs), len(ks)
+        self.counters.mul_pc += S * K
+        self.counters.add_cc += S * (K - 1)
+        depth = max(r.depth for r in rotated) + 1
+        adepth = max(r.assembly_depth for r in rotated)
+        if not rotated[0].tracked:
+            return [SlotCiphertext(None, depth, rotated[0].params, adepth) for _ in pvs]
+        if any(p is None for p in pvs):
+            raise ValueError("tracked ciphertext requires a plaintext operand")
+        two_n = 4 * self.params.n_slots
+        gs = [pow(5, k, two_n) for k in ks]
+        level = min(r.handle.level for r in rotated)
+        hs = []
+        for r in rotated:
+            h = r.handle
+            while h.level > level:
+                h = self.evaluator.mod_switch(h)
+            hs.append(h)
+        outs = self.evaluator.hoisted_dot(hs, gs, [self._device_pt(p) for p in pvs])
+        return [self._wrap(o, depth, adepth) for o in outs]
 
     def rotate_multi(self, cts, ks):
         """rotate(cts[i], ks[i]) for every i: same counters and results, one

@@ -225,6 +225,14 @@ class Evaluator:
                       handle_array([o.ptr for o in outs]), arr, len(cts))
         return outs
 
+    def hoisted_dot(self, R, gs, pts) -> list[Ciphertext]:
+        """out[s] = sum_k R[k] * tau_{gs[k]}(pts[s])."""
+        outs = [self.new_ct(R[0].rows, R[0].level) for _ in pts]
+        arr = (ctypes.c_uint32 * len(gs))(*[int(g) for g in gs])
+        self.lib.call("fhe_hoisted_dot", self.ctx, handle_array([r.ptr for r in R]), arr, len(R),
+                      handle_array([p.ptr for p in pts]), len(pts), handle_array([o.ptr for o in outs]))
+        return outs
+
     def mul_plain_many(self, cts, pts) -> list[Ciphertext]:
         outs = [self.new_ct(c.rows, c.level) for c in cts]
         self.lib.call("fhe_mul_plain_many", self.ctx, handle_array([c.ptr for c in cts]),

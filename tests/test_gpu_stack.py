@@ -66,3 +66,33 @@ def test_cfg0_end_to_end_on_gpu(cuda_lib):
     c = res.counters
     assert (c.mul_pc, c.add_cc, c.rot, c.mul_cc, c.assembly_mul_pc) == (458, 4894, 4889, 2, 438)
     assert min(ctx.noise_budget(ct) for ct in res.value.cts) > 5
+
+
+def test_hoisted_schedule_on_gpu(cuda_lib, golden_lib):
+    """schedule='hoisted': same logits as the reference, ciphertexts equal the
+    golden model's word for word (k_hoisted_dot vs the golden loop)."""
+    for fx in load("networks.json")[:4]:
+        net, ws = network_from_fixture(fx)
+        plan = build_plan(net, "explicit")
+        x = np.array(fx["inputs"])
+        gpu = HeContext(net.scheme, batch=2, lib=cuda_lib, schedule="hoisted", hoist_levels=3)
+        gold = HeContext(net.scheme, batch=2, lib=golden_lib, schedule="hoisted", hoist_levels=3)
+        a = run_encrypted(net, plan, ws, x, ctx=gpu)
+        b = run_encrypted(net, plan, ws, x, ctx=gold)
+        assert [[int(v) for v in row] for row in a.logits] == fx["logits"]
+        for u, v in zip(a.value.cts, b.value.cts):
+            assert np.array_equal(gpu.evaluator.read(u.handle), gold.evaluator.read(v.handle))
+
+
+def test_cfg0_hoisted_on_gpu(cuda_lib):
+    from paper_2102_03494_b200.hesim import SchemeParams
+    net0, ws, xs, meta = cfg0_network(SchemeParams(n_slots=8192, t=(1 << 61) - 1))
+    rp = inference_params(net0, build_plan(net0, "explicit"), ws, input_bound=255)
+    net, _, _, _ = cfg0_network(scheme_for(rp))
+    plan = build_plan(net, "explicit")
+    ctx = HeContext(net.scheme, batch=2, lib=cuda_lib, schedule="hoisted")
+    res = run_encrypted(net, plan, ws, xs, ctx=ctx)
+    for row, want in zip(res.logits, meta["logits"]):
+        assert [str(int(v)) for v in row] == want
+    assert res.counters.rot < 4889 // 2
+    assert min(ctx.noise_budget(ct) for ct in res.value.cts) > 5
