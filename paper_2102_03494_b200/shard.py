@@ -31,10 +31,18 @@ def _words_tensor(ev, ct, device):
     return torch.empty(ev.words(ct), dtype=torch.int64, device=device)
 
 
+def _stream_sync(device):
+    """NCCL ops run on torch's current stream; the library copies on its own
+    stream, so order them explicitly (no-op for CPU tensors / gloo)."""
+    import torch
+    if str(device).startswith("cuda"):
+        torch.cuda.current_stream(torch.device(device)).synchronize()
+
+
 def send_ct(ev, ct, dst: int, device):
     import torch.distributed as dist
     buf = _words_tensor(ev, ct, device)
-    ev.export_words(ct, buf.data_ptr())
+    ev.export_words(ct, buf.data_ptr())        # synchronous on the library stream
     dist.send(buf, dst)
 
 
@@ -43,6 +51,7 @@ def recv_ct(ev, rows: int, level: int, src: int, device):
     ct = ev.new_ct(rows, level)
     buf = _words_tensor(ev, ct, device)
     dist.recv(buf, src)
+    _stream_sync(device)                       # the received words must land before the copy-in
     ev.import_words(ct, buf.data_ptr())
     return ct
 
