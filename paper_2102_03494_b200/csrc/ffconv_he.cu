@@ -910,14 +910,16 @@ extern "C" int fhe_encrypt(fhe_ctx *c, const uint64_t *slots, uint32_t nonce, fh
     CU(cudaMemcpyAsync(s_dev, slots, cnt * n * 8, cudaMemcpyHostToDevice, c->st));
     TRY(slots_to_coef(c, s_dev, m, (int)cnt, ct->R));
     long long total = (long long)cnt * L * n;
-    EW(k_enc_prep, total, m, tmp, total, (int)L, (int)ct->R, (int)c->logn, c->P.seed, nonce, c->d_lv + L, c->t_id0,
+    const long long total8 = (long long)cnt * ((n + 7) / 8);
+    EW(k_enc_prep, total8, m, tmp, total8, (int)L, (int)ct->R, (int)c->logn, c->P.seed, nonce, c->d_lv + L, c->t_id0,
        c->d_mods);
     CHECK_LAUNCH();
     NttRowsArgs a = nargs(tmp, tmp, n);
     a.period = L;
     map_q(a.map, L);
     TRY(ntt_rows(c, (int)(cnt * L), a));
-    EW(k_enc_finish, total, tmp, ct->d, c->d_s_m, total, (int)L, (int)c->logn, c->P.seed, nonce, c->d_mods);
+    const long long total4 = (long long)cnt * L * ((n + 3) / 4);
+    EW(k_enc_finish, total4, tmp, ct->d, c->d_s_m, total4, (int)L, (int)c->logn, c->P.seed, nonce, c->d_mods);
     CHECK_LAUNCH();
     CU(cudaStreamSynchronize(c->st));
     return 0;

@@ -384,39 +384,62 @@ __global__ void k_scaled_msg(const u64 *__restrict__ m, u64 *__restrict__ out, l
     }
 }
 
-// encryption, before the NTT: tmp[ci][i] = e_ci mod q_i + round(Q m / t)
-__global__ void k_enc_prep(const u64 *__restrict__ m, u64 *__restrict__ tmp, long long total, int L, int R,
+// encryption, before the NTT: tmp[ci][i] = e_ci mod q_i + round(Q m / t).
+// One thread per 8 coefficients of one ciphertext: a single ChaCha20 block gives
+// their 8 CBD errors (words 2(c%8), 2(c%8)+1 of block c/8), reused for every limb.
+__global__ void k_enc_prep(const u64 *__restrict__ m, u64 *__restrict__ tmp, long long total8, int L, int R,
                            int logn, u64 seed, u32 nonce, const LevelDev *__restrict__ T, int t_id0,
                            const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
-    GRID_STRIDE(idx, total) {
-        const long long row = idx >> logn;                 // ci * L + i
-        const int i = (int)(row % L);
-        const u32 ci = (u32)(row / L);
+    GRID_STRIDE(idx, total8) {
+        const long long per = (n + 7) >> 3;               // 8-coefficient groups per ciphertext
+        const u32 ci = (u32)(idx / per);
+        const u32 x0 = (u32)(idx % per) * 8;
         const int k = (int)(ci / R);
-        const u32 x = (u32)(idx & (n - 1));
-        const ModInfo &M = mods[i];
-        const int e = sample_cbd(seed, DOM_ENC_E, 0, nonce, ci, x);
-        const u64 sm_ = scaled_msg(*T, k, mods[t_id0 + k].q, m[(long long)ci * n + x], i, M);
-        tmp[idx] = addm(smod(e, M), sm_, M.q);
+        u32 blk[16];
+        chacha_block(blk, seed, x0 >> 3, DOM_ENC_E, 0, nonce, ci);
+        int e[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++)
+            e[u] = __popc(blk[2 * u] & 0x1FFFFFu) - __popc(blk[2 * u + 1] & 0x1FFFFFu);
+        const u64 t = mods[t_id0 + k].q;
+        for (int i = 0; i < L; i++) {
+            const ModInfo &M = mods[i];
+            u64 *dst = tmp + ((long long)ci * L + i) * n + x0;
+#pragma unroll
+            for (int u = 0; u < 8; u++)
+                if (x0 + u < n) dst[u] = addm(smod(e[u], M), scaled_msg(*T, k, t, m[(long long)ci * n + x0 + u], i, M), M.q);
+        }
     }
 }
 
-// encryption, after the NTT: c1 = a (uniform, NTT domain), c0 = tmp - a*s
+// encryption, after the NTT: c1 = a (uniform, NTT domain), c0 = tmp - a*s.
+// One thread per 4 coefficients of one (ciphertext, limb): one ChaCha20 block
+// gives their four 128-bit uniform draws.
 __global__ void k_enc_finish(const u64 *__restrict__ tmp, u64 *__restrict__ ct, const u64 *__restrict__ s_m,
-                             long long total, int L, int logn, u64 seed, u32 nonce, const ModInfo *__restrict__ mods) {
+                             long long total4, int L, int logn, u64 seed, u32 nonce, const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
-    GRID_STRIDE(idx, total) {
-        const long long row = idx >> logn;
+    GRID_STRIDE(idx, total4) {
+        const long long per = (n + 3) >> 2;
+        const long long row = idx / per;                   // ci * L + i
         const int i = (int)(row % L);
         const u32 ci = (u32)(row / L);
-        const u32 x = (u32)(idx & (n - 1));
+        const u32 x0 = (u32)(idx % per) * 4;
         const ModInfo &M = mods[i];
-        const u64 a = sample_uniform(M, seed, DOM_ENC_A, i, nonce, ci, x);
-        const u64 as = mont(a, s_m[(long long)i * n + x], M.q, M.qinv);
+        u32 blk[16];
+        chacha_block(blk, seed, x0 >> 2, DOM_ENC_A, i, nonce, ci);
         u64 *c = ct + ((long long)ci * 2 * L) * n;
-        c[((long long)0 * L + i) * n + x] = subm(tmp[idx], as, M.q);
-        c[((long long)1 * L + i) * n + x] = a;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const u32 x = x0 + u;
+            if (x >= n) break;
+            const u128 v = ((u128)blk[4 * u + 3] << 96) | ((u128)blk[4 * u + 2] << 64) | ((u128)blk[4 * u + 1] << 32) |
+                           blk[4 * u];
+            const u64 a = mod128(v, M);
+            const u64 as = mont(a, s_m[(long long)i * n + x], M.q, M.qinv);
+            c[((long long)0 * L + i) * n + x] = subm(tmp[row * n + x], as, M.q);
+            c[((long long)1 * L + i) * n + x] = a;
+        }
     }
 }
 
