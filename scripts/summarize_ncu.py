@@ -76,7 +76,8 @@ def report(rep, out):
 
 
 if __name__ == "__main__":
-    launches(sys.argv[1], sys.argv[2] + "_launches.txt")
+    if sys.argv[1] != "/dev/null":
+        launches(sys.argv[1], sys.argv[2] + "_launches.txt")
     for rep in sys.argv[3:]:
         tag = rep.split("/")[-1].replace(".ncu-rep", "")
         report(rep, f"{sys.argv[2]}_{tag}.txt")
