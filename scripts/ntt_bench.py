@@ -11,7 +11,7 @@ ev.lib.call("fhe_peak_modmul", ev.ctx, 20000, ctypes.byref(peak))
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 1184
 out = {"peak_gmodmul": peak.value / 1e9, "rows": rows}
 WS = os.environ.get("WS")
-plan = ((0, tuple(int(w) for w in WS.split(","))),) if WS else ((0, (4, 5, 100)), (1, (4, 5, 100)))
+plan = tuple((inv, tuple(int(w) for w in WS.split(","))) for inv in (0, 1)) if WS else ((0, (4, 5, 100)), (1, (4, 5, 100)))
 for inv, Ws in plan:
     for W in Ws:
         ms, bad = ctypes.c_float(), ctypes.c_uint32()
