@@ -52,7 +52,7 @@ extern "C" {
 #define FHE_ELEVEL -4
 
 typedef struct fhe_params {
-    uint32_t log_n;   /* ring degree n = 2^log_n (3 <= log_n <= 14); N = n/2 slots per row */
+    uint32_t log_n;   /* ring degree n = 2^log_n (2 <= log_n <= 16; 2^15, 2^16 rows run on CTA clusters); N = n/2 slots per row */
     uint32_t L;       /* ciphertext primes at the top level                              */
     uint32_t K;       /* special primes (must be 1)                                      */
     uint32_t n_aux;   /* auxiliary base size for fhe_square (0 disables squaring)         */

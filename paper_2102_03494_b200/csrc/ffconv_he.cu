@@ -217,7 +217,7 @@ template <int LOGN, bool INV = false, typename... KArgs, typename... Args>
 static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim3 grid, cudaStream_t st,
                        Args... args) {
     ProfScope ps_(c, name);
-    using C = NttCfg<LOGN, INV ? DefaultWInv<LOGN>::value : DefaultW<LOGN>::value>;
+    using C = RowCfg<LOGN, INV>;
     const size_t smem = (size_t)C::SMEM_WORDS * sizeof(u64);
     {
         std::lock_guard<std::mutex> lk(g_attr_mu);
@@ -226,7 +226,25 @@ static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim
             g_attr_done.insert((const void *)kern);
         }
     }
-    kern<<<grid, C::TH, smem, st>>>(args...);
+    if constexpr (C::CR == 1) {
+        kern<<<grid, C::TH, smem, st>>>(args...);
+    } else {
+        // one thread-block cluster of CR CTAs per row (distributed shared memory)
+        grid.x *= C::CR;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(C::TH);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C::CR;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+    }
 }
 
 #define LOGN_SWITCH(logn, ...)                                   \
@@ -244,6 +262,8 @@ static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim
         case 12: { constexpr int LG = 12; __VA_ARGS__; } break;  \
         case 13: { constexpr int LG = 13; __VA_ARGS__; } break;  \
         case 14: { constexpr int LG = 14; __VA_ARGS__; } break;  \
+        case 15: { constexpr int LG = 15; __VA_ARGS__; } break;  \
+        case 16: { constexpr int LG = 16; __VA_ARGS__; } break;  \
         default: break;                                          \
     }
 
@@ -287,7 +307,7 @@ static int ensure_tmp(fhe_ctx *c, size_t words) {
 
 // ------------------------------------------------------------- validation
 static int validate(const fhe_params *p) {
-    if (p->log_n < 2 || p->log_n > 14) return fail(FHE_EINVAL, "log_n must be in [2, 14] (got %u)", p->log_n);
+    if (p->log_n < 2 || p->log_n > 16) return fail(FHE_EINVAL, "log_n must be in [2, 16] (got %u)", p->log_n);
     if (p->L < 1 || p->L > FHE_MAX_Q) return fail(FHE_EINVAL, "L must be in [1, %d]", FHE_MAX_Q);
     if (p->K != 1) return fail(FHE_EINVAL, "exactly one special prime is supported (K=%u)", p->K);
     if (p->n_aux > FHE_MAX_B) return fail(FHE_EINVAL, "n_aux must be <= %d", FHE_MAX_B);
@@ -491,6 +511,7 @@ static int setup_workspace(fhe_ctx *c) {
     size_t budget = 512ull << 20;
     const char *env = getenv("FHE_KS_BATCH");
     int S = env ? atoi(env) : (int)(budget / per_ct);
+    if (!env && S < 8) S = 8;          // large rings: keep >= 8 ciphertexts per sub-batch
     if (S < 1) S = 1;
     if (S > MAXS) S = MAXS;
     c->S = S;

@@ -66,10 +66,10 @@ struct NttRowsArgs {
 DEV long long row_off(int r, u32 rdiv, long long A, long long B) { return (long long)(r / rdiv) * A + (long long)(r % rdiv) * B; }
 
 template <int LOGN>
-__global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_ntt_rows(NttRowsArgs a, const ModInfo *__restrict__ mods) {
-    using C = FwdCfg<LOGN>;
+__global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_ntt_rows(NttRowsArgs a, const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false>;
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x, tid = threadIdx.x;
+    const int r = C::row(), tid = threadIdx.x, base = C::base();
     const ModInfo M = mods[a.map.id[(r / a.div) % a.period]];
     const u64 *src = a.src + row_off(r, a.rdiv, a.sA, a.sB);
     u64 v[C::E];
@@ -81,14 +81,14 @@ __global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_ntt_rows(NttRowsArgs a, co
     }
 #pragma unroll
     for (int e = 0; e < C::E; e++) {
-        u64 x = src[(e << (LOGN - C::W)) | tid];
+        u64 x = src[C::io(tid, e)];
         if (a.load == 1) x = red64(x, M.q, M.mu);
         else if (a.load == 2) x = centered_lift(x, half_src, msrc_q, M);
         v[e] = x;
     }
-    ntt_fwd_core<LOGN>(v, sm, M, tid);
-    u64 *dst = a.dst + row_off(r, a.rdiv, a.dA, a.dB);
-    for (int i = tid; i < C::N; i += C::TH) {
+    ntt_fwd_row<LOGN>(v, sm, M, tid);
+    u64 *dst = a.dst + row_off(r, a.rdiv, a.dA, a.dB) + base;
+    for (int i = tid; i < C::NL; i += C::TH) {
         u64 x = sm[C::pad(i)];
         if (a.epi == 1) x = to_mont(x, M);
         else if (a.epi == 2) x = addm(dst[i], x, M.q);
@@ -112,14 +112,15 @@ struct InttRowsArgs {
 };
 
 template <int LOGN>
-__global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_intt_rows(InttRowsArgs a, const ModInfo *__restrict__ mods) {
-    using C = InvCfg<LOGN>;
+__global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_intt_rows(InttRowsArgs a, const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, true>;
     extern __shared__ u64 sm[];
-    const int r = blockIdx.x, tid = threadIdx.x;
+    const int r = C::row(), tid = threadIdx.x, base = C::base();
     const ModInfo M = mods[a.map.id[(r / a.div) % a.period]];
     const u64 *src = a.src + row_off(r, a.rdiv, a.sA, a.sB);
-    if (a.gather == 2) {
-        for (int i = tid; i < C::N; i += C::TH) sm[C::pad(i)] = src[i];
+    if (a.gather == 2 && C::CL == 0) {
+        // single-CTA row: stage, then permute inside shared memory
+        for (int i = tid; i < C::NL; i += C::TH) sm[C::pad(i)] = src[i];
         __syncthreads();
         u64 w[C::E];
 #pragma unroll
@@ -128,18 +129,19 @@ __global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_intt_rows(InttRowsArgs a, 
 #pragma unroll
         for (int e = 0; e < C::E; e++) sm[C::pad(tid + e * C::TH)] = w[e];
     } else {
-        for (int i = tid; i < C::N; i += C::TH) {
-            u64 x = a.gather == 1 ? src[a.tab[i]] : src[i];
+        for (int i = tid; i < C::NL; i += C::TH) {
+            const int gi = base + i;
+            u64 x = a.gather == 1 ? src[a.tab[gi]] : a.gather == 2 ? src[galois_perm(gi, a.g, LOGN)] : src[gi];
             if (a.reduce) x = red64(x, M.q, M.mu);
             sm[C::pad(i)] = x;
         }
     }
     __syncthreads();
     u64 v[C::E];
-    ntt_inv_core<LOGN>(v, sm, M, tid);
+    ntt_inv_row<LOGN>(v, sm, M, tid);
     u64 *dst = a.dst + row_off(r, a.rdiv, a.dA, a.dB);
 #pragma unroll
-    for (int e = 0; e < C::E; e++) dst[(e << (LOGN - C::W)) | tid] = v[e];
+    for (int e = 0; e < C::E; e++) dst[C::io(tid, e)] = v[e];
 }
 
 struct PtrTab {
@@ -153,24 +155,35 @@ struct PtrTab {
 // gather on the way out (C1p[s][i]: NTT-form digit for the inner-product
 // diagonal) and on the first inverse-NTT pass (D[s][i]: coefficient digit).
 template <int LOGN>
-__global__ void __launch_bounds__(InvCfg<LOGN>::TH) k_rot_gather_intt(PtrTab pt, int l, u64 *C1p, u64 *D,
-                                                                  const ModInfo *__restrict__ mods) {
-    using C = InvCfg<LOGN>;
+__global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_rot_gather_intt(PtrTab pt, int l, u64 *C1p, u64 *D,
+                                                                      const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, true>;
     extern __shared__ u64 sm[];
-    const int s = blockIdx.x, i = blockIdx.y, tid = threadIdx.x;
+    const int s = C::row(), i = blockIdx.y, tid = threadIdx.x, base = C::base();
     const long long n = C::N;
     const u32 g = pt.g[s];
     const u64 *src = pt.in[s] + ((long long)l + i) * n;
-    for (int x = tid; x < C::N; x += C::TH) sm[C::pad(x)] = src[x];
-    __syncthreads();
     u64 *side = C1p + ((long long)s * l + i) * n;
-    for (int x = tid; x < C::N; x += C::TH) side[x] = sm[C::pad(galois_perm(x, g, LOGN))];
     const ModInfo M = mods[i];
     u64 v[C::E];
-    ntt_inv_core<LOGN>(v, sm, M, tid, g);
+    if constexpr (C::CL == 0) {
+        for (int x = tid; x < C::NL; x += C::TH) sm[C::pad(x)] = src[x];
+        __syncthreads();
+        for (int x = tid; x < C::NL; x += C::TH) side[x] = sm[C::pad(galois_perm(x, g, LOGN))];
+        ntt_inv_core<LOGN>(v, sm, M, tid, g);
+    } else {
+        // cluster row: the automorphism gathers across CTAs, so read it from global memory
+        for (int x = tid; x < C::NL; x += C::TH) {
+            const u64 w = src[galois_perm(base + x, g, LOGN)];
+            side[base + x] = w;
+            sm[C::pad(x)] = w;
+        }
+        __syncthreads();
+        ntt_inv_row<LOGN>(v, sm, M, tid);
+    }
     u64 *dst = D + ((long long)s * l + i) * n;
 #pragma unroll
-    for (int e = 0; e < C::E; e++) dst[(e << (LOGN - C::W)) | tid] = v[e];
+    for (int e = 0; e < C::E; e++) dst[C::io(tid, e)] = v[e];
 }
 
 struct DigitTab {
@@ -183,21 +196,21 @@ struct DigitTab {
 // prime i (i == l: the special prime) and transformed; the diagonal i == j is
 // skipped (the inner product reads it from DigitTab.ntt).
 template <int LOGN>
-__global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
-                                                        const ModInfo *__restrict__ mods) {
-    using C = FwdCfg<LOGN>;
+__global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
+                                                             const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false>;
     extern __shared__ u64 sm[];
-    const int s = blockIdx.x, j = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
+    const int s = C::row(), j = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
     if (i == j) return;
     const long long n = C::N;
     const ModInfo M = mods[i == l ? special_id : i];
     const u64 *src = dt.coef[s] + j * n;
     u64 v[C::E];
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = red64(src[(e << (LOGN - C::W)) | tid], M.q, M.mu);
-    ntt_fwd_core<LOGN>(v, sm, M, tid);
-    u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n;
-    for (int x = tid; x < C::N; x += C::TH) dst[x] = sm[C::pad(x)];
+    for (int e = 0; e < C::E; e++) v[e] = red64(src[C::io(tid, e)], M.q, M.mu);
+    ntt_fwd_row<LOGN>(v, sm, M, tid);
+    u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
+    for (int x = tid; x < C::NL; x += C::TH) dst[x] = sm[C::pad(x)];
 }
 
 // Rescale by a dropped prime (ModDown over the special prime, or BFV modulus
@@ -219,10 +232,10 @@ struct RescaleArgs {
 };
 
 template <int LOGN>
-__global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
-    using C = FwdCfg<LOGN>;
+__global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false>;
     extern __shared__ u64 sm[];
-    const int s = blockIdx.x, p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
+    const int s = C::row(), p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x, gb = C::base();
     const long long n = C::N;
     const ModInfo M = mods[i];
     const ModInfo &S = mods[a.src_id];
@@ -230,10 +243,10 @@ __global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
     const u64 *r = a.coef[s] + p * a.coef_pstride;
     u64 v[C::E];
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = centered_lift(r[(e << (LOGN - C::W)) | tid], half_src, msrc_q, M);
-    ntt_fwd_core<LOGN>(v, sm, M, tid);
-    const u64 *base = a.base[s] + p * a.base_pstride + i * n;
-    u64 *out = a.out[s] + p * a.out_pstride + i * n;
+    for (int e = 0; e < C::E; e++) v[e] = centered_lift(r[C::io(tid, e)], half_src, msrc_q, M);
+    ntt_fwd_row<LOGN>(v, sm, M, tid);
+    const u64 *base = a.base[s] + p * a.base_pstride + i * n + gb;
+    u64 *out = a.out[s] + p * a.out_pstride + i * n + gb;
     const u64 *add = ((a.add_pmask >> p) & 1) && a.add[s] ? a.add[s] + p * a.add_pstride + i * n : nullptr;
     const u64 f = a.fac[i], fsh = a.fac_sh[i];
     u64 y[C::E];
@@ -244,20 +257,28 @@ __global__ void __launch_bounds__(FwdCfg<LOGN>::TH) k_rescale(RescaleArgs a, con
     }
     const u32 add_g = a.add_g[s];
     if (add && add_g) {
-        __syncthreads();
-        for (int x = tid; x < C::N; x += C::TH) sm[C::pad(x)] = add[x];
-        __syncthreads();
+        if constexpr (C::CL == 0) {
+            __syncthreads();
+            for (int x = tid; x < C::NL; x += C::TH) sm[C::pad(x)] = add[x];
+            __syncthreads();
 #pragma unroll
-        for (int e = 0; e < C::E; e++) {
-            const int x = tid + e * C::TH;
-            y[e] = addm(y[e], sm[C::pad(galois_perm(x, add_g, LOGN))], M.q);
+            for (int e = 0; e < C::E; e++) {
+                const int x = tid + e * C::TH;
+                y[e] = addm(y[e], sm[C::pad(galois_perm(x, add_g, LOGN))], M.q);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < C::E; e++) {
+                const int x = tid + e * C::TH;
+                y[e] = addm(y[e], add[galois_perm(gb + x, add_g, LOGN)], M.q);
+            }
         }
     } else if (add) {
 #pragma unroll
-        for (int e = 0; e < C::E; e++) y[e] = addm(y[e], add[tid + e * C::TH], M.q);
+        for (int e = 0; e < C::E; e++) y[e] = addm(y[e], add[gb + tid + e * C::TH], M.q);
     }
     if (a.acc[s]) {
-        const u64 *acc = a.acc[s] + p * a.acc_pstride + i * n;
+        const u64 *acc = a.acc[s] + p * a.acc_pstride + i * n + gb;
 #pragma unroll
         for (int e = 0; e < C::E; e++) y[e] = addm(y[e], acc[tid + e * C::TH], M.q);
     }

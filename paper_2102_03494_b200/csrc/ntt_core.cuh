@@ -155,3 +155,191 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
     for (int e = 0; e < E; e++) v[e] = shoup(v[e], M.ninv, M.ninv_sh, q);
 }
 
+
+// ------------------------------------------------------------------------------
+// Rows longer than one CTA's shared memory (n = 2^15, 2^16): one thread-block
+// cluster of CR = n / 2^14 CTAs per row; CTA `rank` owns words
+// [rank * 2^14, (rank + 1) * 2^14) in its shared memory (distributed shared memory,
+// DSMEM).  Forward: the first W stages (the only ones whose butterflies span CTAs)
+// run on each thread's own words straight from the global load, the results are
+// stored into their owners' shared memory, and the remaining stages run per CTA
+// as in the single-CTA core.  Inverse: mirror image (local passes, then one pass
+// that reads its words from the owners' shared memory).  Same transform, order and
+// twiddles as the single-CTA cores, so every ring size is bit-identical to the
+// golden model.  For n <= 2^14 RowCfg is the single-CTA configuration (CR = 1).
+#include <cooperative_groups.h>
+
+template <int LOGN, bool INV>
+struct RowCfg {
+    static constexpr int LOGL = LOGN > 14 ? 14 : LOGN;    // log2 words per CTA
+    static constexpr int CL = LOGN - LOGL;                // log2 CTAs per row
+    static constexpr int CR = 1 << CL;
+    using Loc = NttCfg<LOGL, INV ? DefaultWInv<LOGL>::value : DefaultW<LOGL>::value>;
+    static constexpr int W = Loc::W, E = Loc::E, TH = Loc::TH, NL = Loc::N, N = 1 << LOGN;
+    static constexpr int SMEM_WORDS = Loc::SMEM_WORDS;
+    static_assert(CL <= 2 && CL <= W, "rows up to 2^16 words");
+    static DEV int pad(int i) { return Loc::pad(i); }
+    static DEV int rank() {
+        if constexpr (CL > 0) return (int)(blockIdx.x & (CR - 1));
+        else return 0;
+    }
+    static DEV int row() { return (int)(blockIdx.x >> CL); }     // row index (blockIdx.x of the 1-CTA layout)
+    static DEV int base() { return rank() << LOGL; }             // global index of local word 0
+    // global element index of v[e] (forward input / inverse output)
+    static DEV int io(int tid, int e) { return (e << (LOGN - W)) | (rank() * TH + tid); }
+};
+
+template <int LOGN>
+DEV void ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo &M, int tid) {
+    namespace cg = cooperative_groups;
+    using R = RowCfg<LOGN, false>;
+    constexpr int W = R::W, E = R::E, LOGL = R::LOGL, CL = R::CL;
+    const u64 q = M.q, q2 = 2 * q;
+    const int rank = R::rank(), gtid = rank * R::TH + tid;
+    cg::cluster_group cl = cg::this_cluster();
+    // stages 0 .. W-1: the pair partner differs in bit W-1-s of e
+#pragma unroll
+    for (int s = 0; s < W; s++) {
+        const int b = W - 1 - s;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            if (e & (1 << b)) continue;
+            const int e2 = e | (1 << b);
+            const ulonglong2 tw = __ldg(M.tw + (1 << s) + (e >> (W - s)));
+            u64 U = v[e];
+            U = U >= q2 ? U - q2 : U;
+            const u64 V = shoup_lazy(v[e2], tw.x, tw.y, q);
+            v[e] = U + V;
+            v[e2] = U - V + q2;
+        }
+    }
+    cl.sync();   // every CTA of the cluster is resident before remote stores
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int owner = e >> (W - CL);
+        const int local = ((e & ((1 << (W - CL)) - 1)) << (LOGN - W)) | gtid;
+        u64 *dst = cl.map_shared_rank(sm, owner);
+        dst[R::pad(local)] = v[e];
+    }
+    cl.sync();
+    // local stages: global stage s = sl + CL, sl = W - CL .. LOGL - 1
+    constexpr int S0 = W - CL;
+    constexpr int NP = (LOGL - S0 + W - 1) / W;
+#pragma unroll
+    for (int p = 0; p < NP; p++) {
+        const int s0 = S0 + p * W;
+        const int f0 = (LOGL - s0 - W) > 0 ? (LOGL - s0 - W) : 0;
+        const int k = (LOGL - s0) < W ? (LOGL - s0) : W;
+#pragma unroll
+        for (int e = 0; e < E; e++) v[e] = sm[R::pad(fidx<W>(tid, e, f0))];
+        __syncthreads();
+#pragma unroll
+        for (int ls = 0; ls < k; ls++) {
+            const int sl = s0 + ls;
+            const int b = LOGL - sl - 1 - f0;
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                if (e & (1 << b)) continue;
+                const int e2 = e | (1 << b);
+                const u32 g = (1u << (sl + CL)) + ((u32)rank << sl) + ((u32)fidx<W>(tid, e, f0) >> (LOGL - sl));
+                const ulonglong2 tw = __ldg(M.tw + g);
+                u64 U = v[e];
+                U = U >= q2 ? U - q2 : U;
+                const u64 V = shoup_lazy(v[e2], tw.x, tw.y, q);
+                v[e] = U + V;
+                v[e2] = U - V + q2;
+            }
+        }
+        if (p == NP - 1) {
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                u64 x = v[e];
+                x = x >= q2 ? x - q2 : x;
+                v[e] = x >= q ? x - q : x;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < E; e++) sm[R::pad(fidx<W>(tid, e, f0))] = v[e];
+        __syncthreads();
+    }
+}
+
+// In: this CTA's words (global base() + x) canonical in sm[pad(x)], synced.
+// Out: v[e] = a[R::io(tid, e)] canonical, scaled by n^-1; ends with a cluster barrier.
+template <int LOGN>
+DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo &M, int tid) {
+    namespace cg = cooperative_groups;
+    using R = RowCfg<LOGN, true>;
+    constexpr int W = R::W, E = R::E, LOGL = R::LOGL, CL = R::CL, N = R::N;
+    const u64 q = M.q, q2 = 2 * q;
+    const int rank = R::rank(), gtid = rank * R::TH + tid;
+    cg::cluster_group cl = cg::this_cluster();
+    constexpr int LT = LOGL - W + CL;            // local stages lt = 0 .. LT-1
+    constexpr int NP = (LT + W - 1) / W;
+#pragma unroll
+    for (int p = 0; p < NP; p++) {
+        const int lt0 = p * W;
+        const int k = (LT - lt0) < W ? (LT - lt0) : W;
+        const int f0 = lt0 < LOGL - W ? lt0 : LOGL - W;
+#pragma unroll
+        for (int e = 0; e < E; e++) v[e] = sm[R::pad(fidx<W>(tid, e, f0))];
+        __syncthreads();
+#pragma unroll
+        for (int ls = 0; ls < k; ls++) {
+            const int lt = lt0 + ls;
+            const int b = lt - f0;
+#pragma unroll
+            for (int e = 0; e < E; e++) {
+                if (e & (1 << b)) continue;
+                const int e2 = e | (1 << b);
+                const u32 g = (u32)(N >> (lt + 1)) + ((u32)rank << (LOGL - lt - 1)) + ((u32)fidx<W>(tid, e, f0) >> (lt + 1));
+                const ulonglong2 tw = __ldg(M.itw + g);
+                const u64 U = v[e], V = v[e2];
+                const u64 s = U + V;
+                v[e] = s >= q2 ? s - q2 : s;
+                v[e2] = shoup_lazy(U - V + q2, tw.x, tw.y, q);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < E; e++) sm[R::pad(fidx<W>(tid, e, f0))] = v[e];
+        __syncthreads();
+    }
+    cl.sync();   // all local stages of the row are done
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const int owner = e >> (W - CL);
+        const int local = ((e & ((1 << (W - CL)) - 1)) << (LOGN - W)) | gtid;
+        const u64 *src = cl.map_shared_rank(sm, owner);
+        v[e] = src[R::pad(local)];
+    }
+    // stages lt = LOGN - W + b: the pair partner differs in bit b of e
+#pragma unroll
+    for (int b = 0; b < W; b++) {
+        const int lt = LOGN - W + b;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+            if (e & (1 << b)) continue;
+            const int e2 = e | (1 << b);
+            const ulonglong2 tw = __ldg(M.itw + (N >> (lt + 1)) + (e >> (b + 1)));
+            const u64 U = v[e], V = v[e2];
+            const u64 s = U + V;
+            v[e] = s >= q2 ? s - q2 : s;
+            v[e2] = shoup_lazy(U - V + q2, tw.x, tw.y, q);
+        }
+    }
+    cl.sync();   // no CTA leaves or reuses its shared memory while another reads it
+#pragma unroll
+    for (int e = 0; e < E; e++) v[e] = shoup(v[e], M.ninv, M.ninv_sh, q);
+}
+
+// Row-size dispatch used by the row kernels.
+template <int LOGN>
+DEV void ntt_fwd_row(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo &M, int tid) {
+    if constexpr (RowCfg<LOGN, false>::CL == 0) ntt_fwd_core<LOGN>(v, sm, M, tid);
+    else ntt_fwd_cluster<LOGN>(v, sm, M, tid);
+}
+template <int LOGN>
+DEV void ntt_inv_row(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo &M, int tid) {
+    if constexpr (RowCfg<LOGN, true>::CL == 0) ntt_inv_core<LOGN>(v, sm, M, tid);
+    else ntt_inv_cluster<LOGN>(v, sm, M, tid);
+}

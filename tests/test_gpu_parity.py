@@ -20,7 +20,11 @@ CASES = [
     (1024, [786433, 65537], 4, 55),
     (8192, [65537], 5, 55),
     (8192, [1099511922689], 4, 40),
+    # rings 2^15 / 2^16: one row per thread-block cluster of 2 / 4 CTAs (DSMEM NTT)
+    (16384, [65537], 3, 50),
+    (32768, [786433], 3, 50),
 ]
+BIG = CASES[-2:]
 
 
 def _pair(case, golden_lib, cuda_lib):
@@ -120,3 +124,27 @@ def test_rotate_multi_matches_single(golden_lib, cuda_lib):
     cg = gd.new_ct(cts[1].rows)
     gd.write(cg, gp.read(cts[1]))
     assert np.array_equal(gd.read(gd.rotate(cg, 4095)), gp.read(multi[1]))
+
+
+@pytest.mark.parametrize("case", BIG, ids=lambda c: f"N{c[0]}")
+def test_cluster_rings_fused_paths_bit_exact(case, golden_lib, cuda_lib):
+    """Cluster-row paths that gather across CTAs: fused rotate-and-add (automorphism
+    of the addend in the ModDown epilogue) and per-ciphertext keys."""
+    gd, gp, P = _pair(case, golden_lib, cuda_lib)
+    rng = np.random.default_rng(8)
+    N = P.n_slots
+    s = _rand_slots(P, 2, rng)
+    cg = gd.encrypt(s, nonce=5)
+    cc = gp.new_ct(2)
+    gp.write(cc, gd.read(cg))
+    k = N // 4 + 3
+    (og,), (oc,) = gd.rotate_add_many([cg], k), gp.rotate_add_many([cc], k)
+    assert np.array_equal(gd.read(og), gp.read(oc))
+    A = s.astype(object)
+    rolled = np.concatenate([np.roll(A[..., :N], -k, axis=-1), np.roll(A[..., N:], -k, axis=-1)], axis=-1)
+    t = np.array(P.t, dtype=object)[:, None, None]
+    assert np.array_equal(gp.decrypt(oc).astype(object), (A + rolled) % t)
+    ks = [1, N - 1]
+    mg, mc = gd.rotate_multi([cg, cg], ks), gp.rotate_multi([cc, cc], ks)
+    for x, y in zip(mg, mc):
+        assert np.array_equal(gd.read(x), gp.read(y))
