@@ -361,6 +361,111 @@ def cfg0_setup(images: int, seed: int, offset: int = 0):
     return net, plan, ws, xs, rp
 
 
+CIFAR_LAYERS = (
+    # configs[3] as SURVEY.md 8(d) pins it: valid convolutions at 2^15 slots (ring 2^16),
+    # "3x3 low-rank conv 3->8 then 1x1 8->32" = ffconv(d=3, r=8, O=32), x^2, 2x2 avg-pool,
+    # ffconv(d=3, r=16, O=64), x^2, 2x2 avg-pool, FC 2304->10; planner "ffconv-default"
+    dict(kind="ffconv", d=3, stride=1, out_channels=32, rank=8),
+    dict(kind="square"), dict(kind="avgpool", d=2, stride=2),
+    dict(kind="ffconv", d=3, stride=1, out_channels=64, rank=16),
+    dict(kind="square"), dict(kind="avgpool", d=2, stride=2),
+    dict(kind="fc", out_channels=10),
+)
+
+
+def cfg3_setup(images: int, seed: int, offset: int = 0):
+    """BASELINE configs[3] on CIFAR-shaped images: weights N(0, 0.05) -> 8-bit and the
+    first two inputs from the committed fixture (tests/golden/cfg3.npz, made by the
+    reference's own code), further images seeded round(clip(N(0.5, 0.25), 0, 1) * 255);
+    zero biases.  Returns the reference logits of the fixture images in range."""
+    from paper_2102_03494_b200.hesim import SchemeParams
+    from paper_2102_03494_b200.netspec import LayerSpec, NetworkSpec, WeightSet, WeightTensor
+    from paper_2102_03494_b200.packing import TensorShape
+    from paper_2102_03494_b200.planner import build_plan
+    from paper_2102_03494_b200.runner import inference_params, scheme_for
+
+    gold = os.path.join(ROOT, "tests", "golden")
+    with open(os.path.join(gold, "cfg3.json")) as fh:
+        meta = json.load(fh)
+    z = np.load(os.path.join(gold, "cfg3.npz"))
+    layers = tuple(LayerSpec(**d) for d in meta["layers"])
+    shape = TensorShape(32, 32, 3)
+    ws = WeightSet()
+    for name, scale in meta["scales"].items():
+        ws.add(WeightTensor(name, z[name.replace(".", "_")].astype(np.int64), 8, scale))
+    prov = NetworkSpec(SchemeParams(n_slots=meta["n_slots"], t=(1 << 61) - 1), shape, layers)
+    rp = inference_params(prov, build_plan(prov, meta["strategy"]), ws, input_bound=255)
+    net = NetworkSpec(scheme_for(rp), shape, layers)
+    plan = build_plan(net, meta["strategy"])
+    fx = z["inputs"].astype(np.int64)
+    extra = max(0, offset + images - len(fx))
+    rng = np.random.default_rng(seed + 1)
+    more = np.round(np.clip(rng.normal(0.5, 0.25, size=(extra, 3, 32, 32)), 0.0, 1.0) * 255).astype(np.int64)
+    xs = np.concatenate([fx, more])[offset:offset + images]
+    ref = [[int(v) for v in row] for row in meta["logits"]][offset:offset + images]
+    return net, plan, ws, xs, rp, ref
+
+
+def run_cifar(args, rank, world, local_rank):
+    """configs[3] on a bounded sample: `--images` images (default 2 = one row pair)
+    per rank, decrypted logits compared with the reference algorithm."""
+    import torch
+    from paper_2102_03494_b200.abi import cuda_library
+    from paper_2102_03494_b200.hesim import HeContext
+    from paper_2102_03494_b200.runner import pack_input, run_encrypted
+    from paper_2102_03494_b200.shard import shard_range
+    torch.cuda.set_device(local_rank)
+    lib = cuda_library()
+    lo, hi = shard_range(args.images, rank, world)
+    per_rank = hi - lo
+    net, plan, ws, xs, rp, ref_logits = cfg3_setup(per_rank, seed=CFG1["seed"], offset=lo)
+    ctx = HeContext(net.scheme, batch=per_rank, lib=lib, schedule=args.schedule)
+    ev = ctx.evaluator
+    stream_ptr = ctypes.c_void_p()
+    lib.call("fhe_ctx_stream", ev.ctx, ctypes.byref(stream_ptr))
+    stream = torch.cuda.ExternalStream(stream_ptr.value, device=local_rank)
+    packed = pack_input(net, plan, xs, ctx)
+    ev.sync()
+    if world > 1:
+        torch.distributed.barrier()
+    rot0 = ctx.counters.rot
+    cnt0 = ctypes.c_uint64()
+    lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt0))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        res = run_encrypted(net, plan, ws, None, ctx=ctx, packed=packed, decrypt=False)
+        e1.record(stream)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    wall = time.perf_counter() - t0
+    cnt1 = ctypes.c_uint64()
+    lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt1))
+    logits = _decrypt_logits(res, ctx)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{local_rank}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    got = [[int(v) for v in row] for row in np.asarray(logits).tolist()]
+    kb = ctypes.c_uint64()
+    lib.call("fhe_ctx_key_bytes", ev.ctx, ctypes.byref(kb))
+    rots = ctx.counters.rot - rot0
+    return {
+        "images_per_s": args.images / (ms * 1e-3), "ms": ms, "wall_s": wall, "images_per_rank": per_rank,
+        "schedule": args.schedule, "crt_primes": len(rp.t), "L": rp.L, "log_qp": round(rp.log_qp, 1),
+        "ring": rp.n, "logical_rotations": rots,
+        "physical_rotations_per_s": rots * rp.T * ctx.rows / (ms * 1e-3),
+        "gpu_launches": int(cnt1.value - cnt0.value), "key_bytes_resident": int(kb.value),
+        "depth": res.depth, "assembly_depth": res.assembly_depth, "clocks": clk.summary(),
+        # images with a fixture (the reference's run_reference logits): exact comparison
+        "logits_checked": len(ref_logits),
+        "logits_match_reference": got[:len(ref_logits)] == ref_logits if ref_logits else None,
+        "logits_sample": [str(int(v)) for v in np.asarray(logits)[0][:3]],
+    }
+
+
 ABLATION = [
     # (name, first layer spec) -- the configs[4] variants: unfactorized 5x5 conv vs FFConv ranks,
     # each under DensePack and ConvPack, followed by square, fc100, square, fc10
@@ -680,7 +785,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["rotation", "inference", "ablation"], default="rotation")
+    ap.add_argument("--workload", choices=["rotation", "inference", "ablation", "cifar"], default="rotation")
     ap.add_argument("--images", type=int, default=256, help="inference: images per step (whole job)")
     ap.add_argument("--chunk", type=int, default=64, help="inference: images per ciphertext batch")
     ap.add_argument("--no-inference", action="store_true", help="rotation workload: skip the inference sample")
@@ -710,6 +815,23 @@ def main():
                 "dtype": "u64", "data": "synthetic (seeded images)",
                 "config": {"workload": f"configs[4]: {args.images} images, chunks of {args.chunk}"},
                 "variants": abl}), flush=True)
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+        return
+    if args.workload == "cifar":
+        if "--images" not in sys.argv:
+            args.images = 2
+        cf = run_cifar(args, rank, world, local_rank)
+        if rank == 0:
+            print(json.dumps({
+                "metric": "encrypted-image inferences/s (FFConv CIFAR-shaped HECNN, configs[3])",
+                "value": cf["images_per_s"], "unit": "images/s", "n_gpus": world, "steps": 1, "warmup": 0,
+                "ms_per_step": cf["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "u64", "data": "synthetic (seeded N(0.5,0.25) images)",
+                "config": {"workload": f"configs[3] sample: {args.images} images (BASELINE: 64), ring 2^16",
+                           "parallelism": f"dp{world} (image shards, no collective)"},
+                "cifar": cf, "gpu_launches": cf["gpu_launches"], "clocks": cf["clocks"]}), flush=True)
         if world > 1:
             import torch
             torch.distributed.destroy_process_group()

@@ -6,6 +6,7 @@
 // allocations, limb-major [T*R][2][level][n] uint64 in the NTT domain.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -114,6 +115,7 @@ static u64 min_root(u64 q, u32 n) {      // minimal primitive 2n-th root of unit
 // ================================================================== context
 struct KeyBuf {
     u64 *d = nullptr;   // [L][2][L+1][n], Montgomery form
+    u64 last = 0;       // key-use tick of the last launch sequence that referenced it
 };
 
 struct fhe_ctx {
@@ -137,12 +139,18 @@ struct fhe_ctx {
     u64 pinv[MAXQ]{}, pinv_sh[MAXQ]{};
     std::unordered_map<u32, KeyBuf> keys;
     u64 key_bytes = 0;
+    // Keys are regenerated deterministically (seed, Galois element), so the store is a
+    // cache: beyond key_budget bytes the least recently used keys not referenced by
+    // the current launch sequence are freed (configs[3] touches ~7,000 steps).
+    u64 key_budget = 0;
+    u64 key_tick = 1;
+    u64 key_evictions = 0;
     // workspaces (key switching: two ping-pong sets, one per stream)
     int S = 1;                          // key-switching sub-batch
     u64 *w_D = nullptr, *w_C1 = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;   // current set
     u64 *ws_D[2]{}, *ws_C1[2]{}, *ws_Ext[2]{}, *ws_Acc[2]{};
     cudaStream_t streams[2]{};
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_key = nullptr;
     u64 *w_sq = nullptr;
     size_t w_sq_words = 0;
     u64 *w_tmp = nullptr;
@@ -525,6 +533,14 @@ static int setup_workspace(fhe_ctx *c) {
     CU(cudaStreamCreateWithFlags(&c->streams[1], cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&c->ev_key, cudaEventDisableTiming));
+    {
+        // key cache budget: FHE_KEY_BUDGET_MB, default 40 % of device memory
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const char *kenv = getenv("FHE_KEY_BUDGET_MB");
+        c->key_budget = kenv ? (u64)atoll(kenv) << 20 : (u64)(tot / 5 * 2);
+    }
     if (c->nb) {
         size_t l = L, nb = c->nb;
         c->w_sq_words = S * n * (2 * l + 2 * nb + 3 * (l + nb) + 3 * l + 3 * l);
@@ -606,6 +622,7 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
     if (c->streams[1]) { cudaStreamSynchronize(c->streams[1]); cudaStreamDestroy(c->streams[1]); }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_key) cudaEventDestroy(c->ev_key);
     if (c->w_tmp) cudaFreeAsync(c->w_tmp, c->st);
     if (c->st) { cudaStreamSynchronize(c->st); cudaStreamDestroy(c->st); }
     delete c;
@@ -784,13 +801,43 @@ extern "C" int fhe_ctx_key_bytes(fhe_ctx *c, uint64_t *out) {
 // ===================================================================== keys
 static u32 galois_elt(const fhe_ctx *c, u32 k) { return (u32)hm::pw(5, k, 2ull * c->n); }
 
+static int evict_keys(fhe_ctx *c, size_t need) {
+    if (c->key_bytes + need <= c->key_budget) return 0;
+    // free down to 3/4 of the budget in one go (one device sync per eviction round)
+    const u64 target = c->key_budget / 4 * 3;
+    std::vector<std::pair<u64, u32>> lru;
+    for (auto &kv : c->keys)
+        if (kv.second.last < c->key_tick && kv.first != 0) lru.push_back({kv.second.last, kv.first});
+    if (lru.empty()) return 0;                 // everything is pinned: exceed the budget
+    std::sort(lru.begin(), lru.end());
+    CU(cudaDeviceSynchronize());               // in-flight sub-batches may still read them
+    const size_t words = (size_t)c->L * 2 * (c->L + 1) * c->n;
+    for (auto &e : lru) {
+        if (c->key_bytes + need <= target) break;
+        cudaFree(c->keys[e.second].d);
+        c->keys.erase(e.second);
+        c->key_bytes -= words * 8;
+        c->key_evictions++;
+    }
+    return 0;
+}
+
 static int get_key(fhe_ctx *c, u32 kid, const u64 **out) {
     auto it = c->keys.find(kid);
-    if (it != c->keys.end()) { *out = it->second.d; return 0; }
+    if (it != c->keys.end()) {
+        it->second.last = c->key_tick;
+        *out = it->second.d;
+        return 0;
+    }
     size_t n = c->n, L = c->L;
     size_t words = L * 2 * (L + 1) * n;
+    TRY(evict_keys(c, words * 8));
     KeyBuf kb;
     CU(cudaMalloc((void **)&kb.d, words * 8));
+    kb.last = c->key_tick;
+    // generate on stream 0 (the shared w_tmp lives there); the other lane waits for it
+    cudaStream_t caller = c->st;
+    c->st = c->streams[0];
     TRY(ensure_tmp(c, L * (L + 1) * n));
     long long total = (long long)L * (L + 1) * n;
     EW(k_key_prep, total, c->w_tmp, total, (int)L, (int)c->logn, c->P.seed, kid, c->special_id, c->d_mods);
@@ -802,6 +849,13 @@ static int get_key(fhe_ctx *c, u32 kid, const u64 **out) {
     EW(k_key_finish, total, c->w_tmp, kb.d, c->d_s_m, c->d_s_can, c->d_s2_m, c->d_pmod, total, (int)L,
        (int)c->logn, c->P.seed, kid, c->special_id, c->d_mods);
     CHECK_LAUNCH();
+    c->st = caller;
+    if (c->streams[1]) {
+        // every later launch on the other lane (not only the caller's: a cached key is
+        // reused by the next sub-batch without a wait) is ordered after the generation
+        CU(cudaEventRecord(c->ev_key, c->streams[0]));
+        CU(cudaStreamWaitEvent(c->streams[1], c->ev_key, 0));
+    }
     c->keys[kid] = kb;
     c->key_bytes += words * 8;
     *out = kb.d;
@@ -812,6 +866,7 @@ extern "C" int fhe_keygen_rotations(fhe_ctx *c, const uint32_t *steps, uint32_t 
     for (u32 i = 0; i < m; i++) {
         if (steps[i] == 0 || steps[i] >= c->N) return fail(FHE_EINVAL, "rotation step %u outside [1, %u)", steps[i], c->N);
         const u64 *k;
+        c->key_tick++;
         TRY(get_key(c, galois_elt(c, steps[i]), &k));
     }
     return 0;
@@ -833,7 +888,7 @@ extern "C" int fhe_ct_create(fhe_ctx *c, uint32_t R, uint32_t level, fhe_ct **ou
 }
 extern "C" void fhe_ct_destroy(fhe_ct *ct) {
     if (!ct) return;
-    cudaFreeAsync(ct->d, ct->ctx->st);
+    cudaFreeAsync(ct->d, ct->ctx->streams[0]);
     delete ct;
 }
 extern "C" uint32_t fhe_ct_level(const fhe_ct *ct) { return ct->level; }
@@ -877,8 +932,9 @@ extern "C" int fhe_pt_create(fhe_ctx *c, fhe_pt **out) {
 }
 extern "C" void fhe_pt_destroy(fhe_pt *pt) {
     if (!pt) return;
-    cudaFreeAsync(pt->coef_t, pt->ctx->st);
-    cudaFreeAsync(pt->ntt_m, pt->ctx->st);
+    // stream 0 explicitly: a finalizer may run while a call has switched c->st to lane 1
+    cudaFreeAsync(pt->coef_t, pt->ctx->streams[0]);
+    cudaFreeAsync(pt->ntt_m, pt->ctx->streams[0]);
     delete pt;
 }
 
@@ -1127,10 +1183,6 @@ static void use_lane(fhe_ctx *c, int k) {
 static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std::vector<u64 *> &out, u32 l,
                        const std::vector<u32> &g, bool add_input = false) {
     std::vector<const u64 *> keys(in.size());
-    for (size_t i = 0; i < in.size(); i++) {
-        if (i > 0 && g[i] == g[i - 1]) { keys[i] = keys[i - 1]; continue; }
-        TRY(get_key(c, g[i], &keys[i]));
-    }
     size_t n = c->n;
     // (profiling runs single-stream so every kernel is timed in isolation)
     const bool two = in.size() > (size_t)c->S && !c->prof;
@@ -1146,6 +1198,12 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
     for (size_t b0 = 0; b0 < in.size() && !rc; b0 += SB, lane ^= 1) {
         use_lane(c, two ? lane : 0);
         int S = (int)std::min<size_t>(SB, in.size() - b0);
+        c->key_tick++;                       // keys of this sub-batch are pinned
+        for (size_t i = b0; i < b0 + S && !rc; i++) {
+            if (i > b0 && g[i] == g[i - 1]) { keys[i] = keys[i - 1]; continue; }
+            rc = get_key(c, g[i], &keys[i]);
+        }
+        if (rc) break;
         PtrTab pt;
         memset(&pt, 0, sizeof pt);
         for (int s = 0; s < S; s++) { pt.in[s] = in[b0 + s]; pt.out[s] = out[b0 + s]; pt.g[s] = g[b0 + s]; }

@@ -21,6 +21,7 @@ Differences a caller can observe, all deliberate:
 
 from __future__ import annotations
 
+import collections
 import hashlib
 import math
 from dataclasses import dataclass, field, replace
@@ -215,7 +216,10 @@ class HeContext:
         self._levels = levels
         self._q_bits = q_bits
         self._ev = None
-        self._pt_cache = {} if pt_cache else None
+        # device plaintexts by content, LRU-bounded (FHE_PT_CACHE_GB, default 16): the
+        # CIFAR-shaped network scatters ~20,000 distinct plaintexts per image batch
+        self._pt_cache = collections.OrderedDict() if pt_cache else None
+        self._pt_cache_bytes = 0
         if schedule not in ("reference", "hoisted"):
             raise ValueError("schedule must be 'reference' or 'hoisted'")
         # "hoisted": the top hoist_levels levels of rotate-and-sum trees that share
@@ -270,14 +274,24 @@ class HeContext:
 
     def _device_pt(self, pv: PlainVector):
         key = pv.content_key()
-        if self._pt_cache is not None and key in self._pt_cache:
-            return self._pt_cache[key]
+        cache = self._pt_cache
+        if cache is not None and key in cache:
+            cache.move_to_end(key)
+            return cache[key]
         N = self.params.n_slots
         res = self._factor_residues(np.asarray(pv.centered()))          # (T, N)
         both = np.concatenate([res, res], axis=1)                        # replicate to row 1
-        pt = self.evaluator.encode(both)
-        if self._pt_cache is not None:
-            self._pt_cache[key] = pt
+        ev = self.evaluator
+        pt = ev.encode(both)
+        if cache is not None:
+            import os
+            size = ev.T * ev.L * ev.n * 8
+            budget = float(os.environ.get("FHE_PT_CACHE_GB", "16")) * (1 << 30)
+            while cache and self._pt_cache_bytes + size > budget:
+                cache.popitem(last=False)
+                self._pt_cache_bytes -= size
+            cache[key] = pt
+            self._pt_cache_bytes += size
         return pt
 
     def _residues(self, ct: SlotCiphertext):

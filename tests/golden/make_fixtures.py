@@ -18,6 +18,10 @@ GPU box, so tests only ever read the committed fixtures:
                         logits, count-only report, and the reference's own
                         encrypted logits with and without the FC->FC slot-0
                         mask fix
+  cfg3.npz / cfg3.json  BASELINE configs[3] as SURVEY.md 8(d) pins it (valid
+                        convs, 2^15 slots, ffconv-default): weights, two seeded
+                        N(0.5, 0.25) CIFAR-shaped inputs, the reference's
+                        run_reference logits and its count-only report
 """
 
 from __future__ import annotations
@@ -249,6 +253,52 @@ def cfg0(images=2, seed=20210205):
 
 
 
+# ------------------------------------------------------------------ cfg3
+CFG3_LAYERS = (
+    dict(kind="ffconv", d=3, stride=1, out_channels=32, rank=8),
+    dict(kind="square"), dict(kind="avgpool", d=2, stride=2),
+    dict(kind="ffconv", d=3, stride=1, out_channels=64, rank=16),
+    dict(kind="square"), dict(kind="avgpool", d=2, stride=2),
+    dict(kind="fc", out_channels=10),
+)
+
+
+def cfg3(images=2, seed=20210316):
+    rng = np.random.default_rng(seed)
+    layers = tuple(LayerSpec(**d) for d in CFG3_LAYERS)
+    shape = TensorShape(w=32, h=32, c=3)
+    prov = NetworkSpec(scheme=SchemeParams(n_slots=32768, t=(1 << 61)), input_shape=shape, layers=layers)
+    ws = WeightSet()
+    for name, shp in required_tensors(prov).items():
+        if name.endswith(".bias"):
+            ws.add(WeightTensor(name=name, values=np.zeros(shp, dtype=np.int64), bits=8, scale=1.0))
+        else:
+            q, s = quantize_matrix(rng.normal(0.0, 0.05, size=shp), 8)
+            ws.add(WeightTensor(name=name, values=q, bits=8, scale=s))
+    xs = np.round(np.clip(rng.normal(0.5, 0.25, size=(images, 3, 32, 32)), 0.0, 1.0) * 255).astype(np.int64)
+    bounds = [e.static_bound for e in ref_runner.static_bounds(prov, ws, input_bound=255)]
+    logits, maxima = [], None
+    for x in xs:
+        lg, _, mx = ref_runner.run_reference(prov, ws, x)
+        logits.append([str(int(v)) for v in lg])
+        maxima = mx if maxima is None else [max(a, b) for a, b in zip(maxima, mx)]
+    plan = build_plan(prov, "ffconv-default")
+    counts = ref_runner.run_encrypted(prov, plan, ws, None, track_values=False)
+    np.savez_compressed(os.path.join(HERE, "cfg3.npz"), inputs=xs,
+                        **{name.replace(".", "_"): ws[name].values for name in ws.names()})
+    meta = {
+        "seed": seed, "sigma": 0.05, "layers": list(CFG3_LAYERS), "input_shape": [32, 32, 3],
+        "n_slots": 32768, "strategy": "ffconv-default",
+        "scales": {name: ws[name].scale for name in ws.names()},
+        "logits": logits, "layer_max_bits": [round(math.log2(max(m, 1)), 2) for m in maxima],
+        "static_bound_bits": [round(math.log2(max(b, 1)), 2) for b in bounds],
+        "plan": [[st.op, st.layer_index, st.pattern] for st in plan.steps],
+        "count_rows": _rows_json(counts.report), "depth": counts.depth, "assembly_depth": counts.assembly_depth,
+    }
+    with open(os.path.join(HERE, "cfg3.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
 def weight_file():
     """A CPKW0001 file written by the reference (weights.py:102-124)."""
     from cipherpack.weights import save_weights as ref_save
@@ -259,10 +309,14 @@ def weight_file():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["cfg3"]:
+        cfg3()
+        sys.exit(0)
     with open(os.path.join(HERE, "hesim_sequences.json"), "w") as fh:
         json.dump(hesim_sequences(), fh)
     with open(os.path.join(HERE, "networks.json"), "w") as fh:
         json.dump(networks(), fh)
     cfg0()
+    cfg3()
     weight_file()
     print("fixtures written to", HERE)

@@ -148,3 +148,46 @@ def test_cluster_rings_fused_paths_bit_exact(case, golden_lib, cuda_lib):
     mg, mc = gd.rotate_multi([cg, cg], ks), gp.rotate_multi([cc, cc], ks)
     for x, y in zip(mg, mc):
         assert np.array_equal(gd.read(x), gp.read(y))
+
+
+@pytest.mark.parametrize("case", [CASES[2], BIG[1]], ids=lambda c: f"N{c[0]}")
+def test_key_cache_eviction_bit_exact(case, golden_lib, cuda_lib, monkeypatch):
+    """Rotation keys are regenerated on demand: with a key budget of a few keys,
+    many distinct steps (per-ciphertext keys, several sub-batches) still give the
+    golden model's words."""
+    n_slots, t, L, qb = case
+    P = make_params(n_slots, t, levels=L, q_bits=qb)
+    key_mb = L * 2 * (L + 1) * 2 * n_slots * 8 / 2 ** 20
+    monkeypatch.setenv("FHE_KEY_BUDGET_MB", str(max(1, int(3 * key_mb))))
+    monkeypatch.setenv("FHE_KS_BATCH", "4")
+    gd, gp = Evaluator(P, golden_lib), Evaluator(P, cuda_lib)
+    rng = np.random.default_rng(9)
+    s = _rand_slots(P, 1, rng)
+    cg = gd.encrypt(s, nonce=11)
+    cc = gp.new_ct(1)
+    gp.write(cc, gd.read(cg))
+    N = P.n_slots
+    ks = [int(k) for k in rng.choice(np.arange(1, N), size=14, replace=False)]
+    multi = gp.rotate_multi([cc] * len(ks), ks)
+    for k, m in zip(ks, multi):
+        assert np.array_equal(gd.read(gd.rotate(cg, k)), gp.read(m)), k
+    # evicted keys come back bit-identical
+    again = gp.rotate_multi([cc] * 3, ks[:3])
+    for a, m in zip(again, multi[:3]):
+        assert np.array_equal(gp.read(a), gp.read(m))
+
+
+def test_lane_reuses_fresh_key_bit_exact(golden_lib, cuda_lib, monkeypatch):
+    """A key generated for the first sub-batch (stream 0) and reused from the cache
+    by the next sub-batch on the second stream: the second stream must wait for the
+    generation (ring 2^16, L = 8, sub-batches of 3 physical ciphertexts)."""
+    monkeypatch.setenv("FHE_KS_BATCH", "3")
+    P = make_params(32768, [786433, 1179649], levels=8, q_bits=60, p_bits=61)
+    gd, gp = Evaluator(P, golden_lib), Evaluator(P, cuda_lib)
+    rng = np.random.default_rng(12)
+    s = _rand_slots(P, 6, rng)
+    cg = gd.encrypt(s, nonce=3)
+    cc = gp.new_ct(6)
+    gp.write(cc, gd.read(cg))
+    for k in (1, 12345):
+        assert np.array_equal(gd.read(gd.rotate(cg, k)), gp.read(gp.rotate(cc, k))), k
