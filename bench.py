@@ -432,6 +432,9 @@ def run_cifar(args, rank, world, local_rank):
     cnt0 = ctypes.c_uint64()
     lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt0))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = os.environ.get("FHE_BENCH_PROF") == "1"      # per-kernel breakdown (single stream, slower)
+    if prof:
+        lib.call("fhe_prof_enable", ev.ctx, 1)
     t0 = time.perf_counter()
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
@@ -441,6 +444,12 @@ def run_cifar(args, rank, world, local_rank):
         e1.synchronize()
     ms = e0.elapsed_time(e1)
     wall = time.perf_counter() - t0
+    breakdown = None
+    if prof:
+        buf = ctypes.create_string_buffer(1 << 16)
+        lib.call("fhe_prof_report", ev.ctx, buf, len(buf))
+        lib.call("fhe_prof_enable", ev.ctx, 0)
+        breakdown = {k: {"calls": c, "ms": round(m, 3)} for k, (c, m) in parse_prof(buf.value.decode()).items()}
     cnt1 = ctypes.c_uint64()
     lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt1))
     logits = _decrypt_logits(res, ctx)
@@ -463,6 +472,7 @@ def run_cifar(args, rank, world, local_rank):
         "logits_checked": len(ref_logits),
         "logits_match_reference": got[:len(ref_logits)] == ref_logits if ref_logits else None,
         "logits_sample": [str(int(v)) for v in np.asarray(logits)[0][:3]],
+        "kernel_ms": breakdown,
     }
 
 

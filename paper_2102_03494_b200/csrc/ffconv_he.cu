@@ -145,6 +145,11 @@ struct fhe_ctx {
     u64 key_budget = 0;
     u64 key_tick = 1;
     u64 key_evictions = 0;
+    std::vector<u64 *> key_free;        // buffers of evicted keys, reused (cudaFree is slow and synchronizing)
+    // pinned staging for plaintext encoding (two slots, so encode never waits for the stream)
+    u64 *enc_stage[2]{};
+    cudaEvent_t enc_ev[2]{};
+    int enc_next = 0;
     // workspaces (key switching: two ping-pong sets, one per stream)
     int S = 1;                          // key-switching sub-batch
     u64 *w_D = nullptr, *w_C1 = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;   // current set
@@ -612,6 +617,11 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
     cudaSetDevice(c->dev);
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto &kv : c->keys) cudaFree(kv.second.d);
+    for (u64 *d : c->key_free) cudaFree(d);
+    for (int j = 0; j < 2; j++) {
+        if (c->enc_stage[j]) cudaFreeHost(c->enc_stage[j]);
+        if (c->enc_ev[j]) cudaEventDestroy(c->enc_ev[j]);
+    }
     void *bufs[] = {c->d_mods, c->d_tw, c->d_s_can, c->d_s_m, c->d_s2_m, c->d_sk_ids, c->d_slot2ntt,
                     c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_sq};
     for (void *b : bufs) if (b) cudaFree(b);
@@ -814,7 +824,7 @@ static int evict_keys(fhe_ctx *c, size_t need) {
     const size_t words = (size_t)c->L * 2 * (c->L + 1) * c->n;
     for (auto &e : lru) {
         if (c->key_bytes + need <= target) break;
-        cudaFree(c->keys[e.second].d);
+        c->key_free.push_back(c->keys[e.second].d);
         c->keys.erase(e.second);
         c->key_bytes -= words * 8;
         c->key_evictions++;
@@ -833,7 +843,12 @@ static int get_key(fhe_ctx *c, u32 kid, const u64 **out) {
     size_t words = L * 2 * (L + 1) * n;
     TRY(evict_keys(c, words * 8));
     KeyBuf kb;
-    CU(cudaMalloc((void **)&kb.d, words * 8));
+    if (!c->key_free.empty()) {
+        kb.d = c->key_free.back();
+        c->key_free.pop_back();
+    } else {
+        CU(cudaMalloc((void **)&kb.d, words * 8));
+    }
     kb.last = c->key_tick;
     // generate on stream 0 (the shared w_tmp lives there); the other lane waits for it
     cudaStream_t caller = c->st;
@@ -953,7 +968,18 @@ static int slots_to_coef(fhe_ctx *c, const u64 *slots, u64 *coef, int rows, u32 
 extern "C" int fhe_encode(fhe_ctx *c, const uint64_t *slots, fhe_pt *pt) {
     size_t n = c->n;
     TRY(ensure_tmp(c, c->T * n));
-    CU(cudaMemcpyAsync(c->w_tmp, slots, c->T * n * 8, cudaMemcpyHostToDevice, c->st));
+    // host slots -> pinned slot (after its previous copy completed) -> device, asynchronously
+    const int j = c->enc_next;
+    c->enc_next ^= 1;
+    if (!c->enc_stage[j]) {
+        CU(cudaMallocHost((void **)&c->enc_stage[j], c->T * n * 8));
+        CU(cudaEventCreateWithFlags(&c->enc_ev[j], cudaEventDisableTiming));
+    } else {
+        CU(cudaEventSynchronize(c->enc_ev[j]));
+    }
+    memcpy(c->enc_stage[j], slots, c->T * n * 8);
+    CU(cudaMemcpyAsync(c->w_tmp, c->enc_stage[j], c->T * n * 8, cudaMemcpyHostToDevice, c->st));
+    CU(cudaEventRecord(c->enc_ev[j], c->st));
     TRY(slots_to_coef(c, c->w_tmp, pt->coef_t, (int)c->T, 1));
     // centered lift t_k -> q_i, NTT, Montgomery form; row r = k*L + i
     NttRowsArgs a = nargs(pt->coef_t, pt->ntt_m, 0);
@@ -962,8 +988,6 @@ extern "C" int fhe_encode(fhe_ctx *c, const uint64_t *slots, fhe_pt *pt) {
     a.div2 = c->L; a.period2 = c->T; map_range(a.srcmap, c->T, c->t_id0);
     a.load = 2; a.epi = 1;
     TRY(ntt_rows(c, (int)(c->T * c->L), a));
-    // the host buffer must outlive the copy
-    CU(cudaStreamSynchronize(c->st));
     pt->encoded = 1;
     return 0;
 }

@@ -120,14 +120,30 @@ class PlainVector:
     The device encoding is created on first use and cached by content.
     """
 
-    __slots__ = ("slots", "params", "_key")
+    __slots__ = ("_slots", "params", "_key", "_small")
 
-    def __init__(self, slots: np.ndarray, params: SchemeParams):
-        self.slots = slots
+    def __init__(self, slots: np.ndarray | None, params: SchemeParams, small: np.ndarray | None = None):
+        # `small`: the same vector as centered int64 values when every |v| < 2^62 (weights,
+        # masks); the canonical residue array is then built only if someone asks for it
+        self._slots = slots
         self.params = params
         self._key = None
+        self._small = small
+
+    @property
+    def slots(self) -> np.ndarray:
+        if self._slots is None:
+            t = self.params.t
+            if self.params.int64_storage:
+                self._slots = np.mod(self._small, t).astype(np.int64)
+            else:
+                v = self._small.astype(object)
+                self._slots = np.where(v < 0, v + t, v)
+        return self._slots
 
     def centered(self) -> np.ndarray:
+        if self._small is not None:
+            return self._small
         lift = (self.params.t + 1) // 2
         out = self.slots.astype(np.int64, copy=True) if self.params.int64_storage else self.slots.copy()
         out[self.slots >= lift] -= self.params.t
@@ -135,10 +151,19 @@ class PlainVector:
 
     def content_key(self) -> bytes:
         if self._key is None:
-            arr = np.asarray(self.slots)
-            if arr.dtype == object:
-                arr = np.array([str(int(v)) for v in arr]).astype("S")
-            self._key = hashlib.blake2b(arr.tobytes(), digest_size=16).digest()
+            if self._small is not None:
+                data = b"i64" + self._small.tobytes()
+            else:
+                arr = np.asarray(self.slots)
+                if arr.dtype == object:
+                    c = self.centered()
+                    if all(abs(int(x)) < 2 ** 62 for x in (c.min(), c.max())):
+                        data = b"i64" + c.astype(np.int64).tobytes()
+                    else:
+                        data = np.array([str(int(v)) for v in arr]).astype("S").tobytes()
+                else:
+                    data = b"i64" + self.centered().astype(np.int64).tobytes()
+            self._key = hashlib.blake2b(data, digest_size=16).digest()
         return self._key
 
 
@@ -324,13 +349,25 @@ class HeContext:
         if values.size > n:
             raise CapacityError(f"{values.size} values exceed {n} slots")
         flat = values.ravel()
-        if flat.size and int(2 * np.max(np.abs(flat.astype(object)))) >= t:
+        if flat.size and flat.dtype != object:
+            if flat.dtype.kind in "ib":
+                big = int(np.max(np.abs(flat.astype(np.int64))))
+            elif flat.dtype.kind == "u":
+                big = int(flat.max())
+            else:
+                big = int(max(abs(int(x)) for x in flat.tolist()))
+        else:
+            big = int(max(abs(int(flat.min())), abs(int(flat.max())))) if flat.size else 0
+        if flat.size and 2 * big >= t:
             raise EncodingOverflowError(f"|value| must be < t/2 = {t / 2}")
+        if not flat.size or big < 2 ** 62:
+            small = np.zeros(n, dtype=np.int64)       # centered values; residues built lazily
+            small[: flat.size] = flat.astype(np.int64)
+            return PlainVector(None, self.params, small=small)
         dtype = np.int64 if self.params.int64_storage else object
         slots = np.zeros(n, dtype=dtype)
-        if flat.size:
-            res = np.asarray(flat, dtype=object) % t
-            slots[: flat.size] = res.astype(np.int64) if self.params.int64_storage else res
+        res = np.asarray(flat, dtype=object) % t
+        slots[: flat.size] = res.astype(np.int64) if self.params.int64_storage else res
         return PlainVector(slots, self.params)
 
     def encrypt(self, values) -> SlotCiphertext:
