@@ -124,7 +124,11 @@ int fhe_pt_read(fhe_ctx *ctx, const fhe_pt *pt, uint64_t *words);
 /* ---- client side ---------------------------------------------------------- */
 /* slots: [T][R][n] residues; secret-key encryption at the top level.  Each call
  * must use a fresh nonce (the randomness is a pure function of seed, nonce and
- * the physical ciphertext index). */
+ * the physical ciphertext index).
+ * Host buffers in page-locked memory (cudaMallocHost / cudaHostRegister) make
+ * fhe_encrypt and fhe_decrypt asynchronous: the copies run on the context's copy
+ * stream and overlap evaluation; the input must stay untouched and the output is
+ * valid only after fhe_sync().  Pageable buffers are copied synchronously. */
 int fhe_encrypt(fhe_ctx *ctx, const uint64_t *slots, uint32_t nonce, fhe_ct *out);
 int fhe_decrypt(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *slots);
 /* diagnostic: coefficient-form x = c0 + c1*s over Q_level, [T*R][level][n]

@@ -146,6 +146,16 @@ struct fhe_ctx {
     u64 key_tick = 1;
     u64 key_evictions = 0;
     std::vector<u64 *> key_free;        // buffers of evicted keys, reused (cudaFree is slow and synchronizing)
+    // copy engine: pinned host buffers in fhe_encrypt / fhe_decrypt are copied on their own
+    // stream through double-buffered device staging, overlapping the compute stream
+    // (separate H2D and D2H streams: PCIe is full duplex; NIO staging slots so a whole
+    // chunked batch can be in flight while the previous one is evaluated)
+    static constexpr int NIO = 8;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    u64 *io_in[NIO]{}, *io_out[NIO]{};
+    size_t io_in_words[NIO]{}, io_out_words[NIO]{};
+    cudaEvent_t ev_in_ready[NIO]{}, ev_in_free[NIO]{}, ev_out_ready[NIO]{}, ev_out_free[NIO]{};
+    int io_in_next = 0, io_out_next = 0;
     // pinned staging for plaintext encoding (two slots, so encode never waits for the stream)
     u64 *enc_stage[2]{};
     cudaEvent_t enc_ev[2]{};
@@ -539,6 +549,14 @@ static int setup_workspace(fhe_ctx *c) {
     CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&c->ev_key, cudaEventDisableTiming));
+    CU(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (int j = 0; j < fhe_ctx::NIO; j++) {
+        CU(cudaEventCreateWithFlags(&c->ev_in_ready[j], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->ev_in_free[j], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->ev_out_ready[j], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->ev_out_free[j], cudaEventDisableTiming));
+    }
     {
         // key cache budget: FHE_KEY_BUDGET_MB, default 40 % of device memory
         size_t fr = 0, tot = 0;
@@ -622,6 +640,14 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
         if (c->enc_stage[j]) cudaFreeHost(c->enc_stage[j]);
         if (c->enc_ev[j]) cudaEventDestroy(c->enc_ev[j]);
     }
+    if (c->h2d) { cudaStreamSynchronize(c->h2d); cudaStreamDestroy(c->h2d); }
+    if (c->d2h) { cudaStreamSynchronize(c->d2h); cudaStreamDestroy(c->d2h); }
+    for (int j = 0; j < fhe_ctx::NIO; j++) {
+        if (c->io_in[j]) cudaFree(c->io_in[j]);
+        if (c->io_out[j]) cudaFree(c->io_out[j]);
+        cudaEvent_t evs[] = {c->ev_in_ready[j], c->ev_in_free[j], c->ev_out_ready[j], c->ev_out_free[j]};
+        for (cudaEvent_t e : evs) if (e) cudaEventDestroy(e);
+    }
     void *bufs[] = {c->d_mods, c->d_tw, c->d_s_can, c->d_s_m, c->d_s2_m, c->d_sk_ids, c->d_slot2ntt,
                     c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_sq};
     for (void *b : bufs) if (b) cudaFree(b);
@@ -640,6 +666,26 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
 
 extern "C" int fhe_sync(fhe_ctx *c) {
     CU(cudaStreamSynchronize(c->st));
+    if (c->h2d) CU(cudaStreamSynchronize(c->h2d));
+    if (c->d2h) CU(cudaStreamSynchronize(c->d2h));
+    return 0;
+}
+
+static bool is_pinned(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// (re)size a device staging buffer once no copy uses it
+static int ensure_stage(fhe_ctx *c, u64 **buf, size_t *have, size_t words) {
+    if (*have >= words) return 0;
+    CU(cudaStreamSynchronize(c->h2d));
+    CU(cudaStreamSynchronize(c->d2h));
+    CU(cudaStreamSynchronize(c->st));
+    if (*buf) CU(cudaFree(*buf));
+    CU(cudaMalloc((void **)buf, words * 8));
+    *have = words;
     return 0;
 }
 
@@ -1008,8 +1054,23 @@ extern "C" int fhe_encrypt(fhe_ctx *c, const uint64_t *slots, uint32_t nonce, fh
     size_t n = c->n, L = c->L, cnt = ct->count;
     TRY(ensure_tmp(c, cnt * n * (2 + L)));
     u64 *s_dev = c->w_tmp, *m = c->w_tmp + cnt * n, *tmp = m + cnt * n;
-    CU(cudaMemcpyAsync(s_dev, slots, cnt * n * 8, cudaMemcpyHostToDevice, c->st));
+    const bool async = is_pinned(slots);
+    int j = 0;
+    if (async) {
+        // pinned input: H2D on the copy stream into staging slot j, the compute stream waits
+        j = c->io_in_next;
+        c->io_in_next = (j + 1) % fhe_ctx::NIO;
+        TRY(ensure_stage(c, &c->io_in[j], &c->io_in_words[j], cnt * n));
+        s_dev = c->io_in[j];
+        CU(cudaStreamWaitEvent(c->h2d, c->ev_in_free[j], 0));
+        CU(cudaMemcpyAsync(s_dev, slots, cnt * n * 8, cudaMemcpyHostToDevice, c->h2d));
+        CU(cudaEventRecord(c->ev_in_ready[j], c->h2d));
+        CU(cudaStreamWaitEvent(c->st, c->ev_in_ready[j], 0));
+    } else {
+        CU(cudaMemcpyAsync(s_dev, slots, cnt * n * 8, cudaMemcpyHostToDevice, c->st));
+    }
     TRY(slots_to_coef(c, s_dev, m, (int)cnt, ct->R));
+    if (async) CU(cudaEventRecord(c->ev_in_free[j], c->st));
     long long total = (long long)cnt * L * n;
     const long long total8 = (long long)cnt * ((n + 7) / 8);
     EW(k_enc_prep, total8, m, tmp, total8, (int)L, (int)ct->R, (int)c->logn, c->P.seed, nonce, c->d_lv + L, c->t_id0,
@@ -1022,7 +1083,7 @@ extern "C" int fhe_encrypt(fhe_ctx *c, const uint64_t *slots, uint32_t nonce, fh
     const long long total4 = (long long)cnt * L * ((n + 3) / 4);
     EW(k_enc_finish, total4, tmp, ct->d, c->d_s_m, total4, (int)L, (int)c->logn, c->P.seed, nonce, c->d_mods);
     CHECK_LAUNCH();
-    CU(cudaStreamSynchronize(c->st));
+    if (!async) CU(cudaStreamSynchronize(c->st));      // pageable input: the host buffer may be reused
     return 0;
 }
 
@@ -1051,6 +1112,20 @@ extern "C" int fhe_decrypt(fhe_ctx *c, const fhe_ct *ct, uint64_t *slots) {
     a.period = c->T;
     map_range(a.map, c->T, c->t_id0);
     TRY(ntt_rows(c, (int)cnt, a));
+    if (is_pinned(slots)) {
+        // pinned output: gather into staging slot j, D2H on the copy stream; valid after fhe_sync
+        const int j = c->io_out_next;
+        c->io_out_next = (j + 1) % fhe_ctx::NIO;
+        TRY(ensure_stage(c, &c->io_out[j], &c->io_out_words[j], cnt * n));
+        CU(cudaStreamWaitEvent(c->st, c->ev_out_free[j], 0));
+        EW(k_gather_slots, total, m, c->io_out[j], total, (int)c->logn, c->d_slot2ntt);
+        CHECK_LAUNCH();
+        CU(cudaEventRecord(c->ev_out_ready[j], c->st));
+        CU(cudaStreamWaitEvent(c->d2h, c->ev_out_ready[j], 0));
+        CU(cudaMemcpyAsync(slots, c->io_out[j], cnt * n * 8, cudaMemcpyDeviceToHost, c->d2h));
+        CU(cudaEventRecord(c->ev_out_free[j], c->d2h));
+        return 0;
+    }
     EW(k_gather_slots, total, m, o, total, (int)c->logn, c->d_slot2ntt);
     CHECK_LAUNCH();
     CU(cudaMemcpyAsync(slots, o, cnt * n * 8, cudaMemcpyDeviceToHost, c->st));
