@@ -162,6 +162,11 @@ int fhe_rotate_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, uint32_t
 int fhe_rotate_add_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t k);
 /* m rotations with their own steps k[i] in [1, N) (e.g. a combine chain) */
 int fhe_rotate_multi(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, const uint32_t *k, uint32_t m);
+/* out[j] = rotate(a, k[j]) for j < m, sharing one digit decomposition + ModUp of a
+ * (hoisted rotations; SURVEY a14 "shared ModUp per source ct"); words equal m
+ * separate fhe_rotate calls.  Replaces the per-destination rotations of one masked
+ * source in the reference's H-Im2Col moves (packing.py:249-279). */
+int fhe_rotate_hoisted(fhe_ctx *ctx, const fhe_ct *a, const uint32_t *k, uint32_t m, fhe_ct *const *out);
 int fhe_mul_plain_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m);
 int fhe_add_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *b, fhe_ct *const *out, uint32_t m);
 

@@ -812,7 +812,8 @@ int fhe_add_plain(fhe_ctx *c, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out) {
 
 /*
  * Hybrid key switching, one prime per digit, one special prime P.
- *   dig_coef[j] : digit j in coefficient form, values in [0, q_j)
+ *   dig_coef[j] : digit j in coefficient form, values in [0, q_j), lifted centered
+ *                 into the other primes
  *   dig_ntt[j]  : the same limb in NTT form (NTT_{q_j}(dig_coef[j]))
  * out0/out1 [l][n] NTT domain: round((sum_j d_j * ksk_j) / P) over Q_l.
  */
@@ -830,8 +831,11 @@ static void keyswitch(fhe_ctx *c, u32 l, const u64 *dig_coef, const u64 *dig_ntt
             if (ii == j) {
                 ext = dig_ntt + (size_t)j * n;
             } else {
+                /* centered lift of the digit (sign-symmetric, so the lift commutes with
+                 * automorphisms: hoisted rotations reproduce these words exactly) */
                 const u64 *d = dig_coef + (size_t)j * n;
-                for (u32 x = 0; x < n; x++) tmp[x] = d[x] % q;
+                const u64 qj = c->P.q[j], hj = (qj - 1) / 2;
+                for (u32 x = 0; x < n; x++) tmp[x] = d[x] > hj ? smod(-(i64)(qj - d[x]), q) : d[x] % q;
                 ntt(tmp, &c->M[pi], n);
                 ext = tmp;
             }
@@ -1077,6 +1081,15 @@ int fhe_rotate_add_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32
 }
 int fhe_rotate_multi(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, const uint32_t *k, uint32_t m) {
     for (u32 i = 0; i < m; i++) { int rc = fhe_rotate(c, a[i], k[i], out[i]); if (rc) return rc; }
+    return 0;
+}
+
+/* hoisting is a device-side cost optimisation; the words are those of separate rotations */
+int fhe_rotate_hoisted(fhe_ctx *c, const fhe_ct *a, const uint32_t *k, uint32_t m, fhe_ct *const *out) {
+    for (uint32_t j = 0; j < m; j++) {
+        int rc = fhe_rotate(c, a, k[j], out[j]);
+        if (rc) return rc;
+    }
     return 0;
 }
 int fhe_mul_plain_many(fhe_ctx *c, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m) {

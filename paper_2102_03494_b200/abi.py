@@ -84,6 +84,7 @@ SIGNATURES = {
     "fhe_square": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fhe_rotate_many": (c_int, [c_void_p, _VPP, _VPP, c_uint32, c_uint32]),
     "fhe_rotate_multi": (c_int, [c_void_p, _VPP, _VPP, POINTER(c_uint32), c_uint32]),
+    "fhe_rotate_hoisted": (c_int, [c_void_p, c_void_p, POINTER(c_uint32), c_uint32, _VPP]),
     "fhe_rotate_add_many": (c_int, [c_void_p, _VPP, _VPP, c_uint32, c_uint32]),
     "fhe_mul_plain_many": (c_int, [c_void_p, _VPP, _VPP, _VPP, c_uint32]),
     "fhe_hoisted_dot": (c_int, [c_void_p, _VPP, POINTER(c_uint32), c_uint32, _VPP, c_uint32, _VPP]),

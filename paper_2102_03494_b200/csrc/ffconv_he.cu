@@ -1210,13 +1210,19 @@ struct KsOut {
     long long acc_pstride;
 };
 
-static int keyswitch_core(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsOut &ko) {
-    size_t n = c->n;
-    int L = (int)c->L;
-    // ModUp: every off-diagonal (digit, prime) pair
+// ModUp: every off-diagonal (digit, prime) pair of S cts into Ext
+static int keyswitch_modup(fhe_ctx *c, int S, u32 l, const DigitTab &dt) {
     LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_modup", k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
                                         c->d_mods));
     CHECK_LAUNCH();
+    return 0;
+}
+
+// inner product with the keys + ModDown (+ epilogue adds) for S items whose extended
+// digits are in Ext (item s reads block s, or dt.esrc[s] through dt.perm[s])
+static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsOut &ko) {
+    size_t n = c->n;
+    int L = (int)c->L;
     // inner-product variant: (ciphertexts per thread, min CTAs per SM); env FHE_KS_VARIANT=0..3
     static int ksv = -1;
     if (ksv < 0) { const char *e = getenv("FHE_KS_VARIANT"); ksv = e ? atoi(e) : 2; }   // 2: measured best (4 cts/thread, 4 CTAs/SM)
@@ -1267,6 +1273,11 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
     CHECK_LAUNCH();
     return 0;
+}
+
+static int keyswitch_core(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsOut &ko) {
+    TRY(keyswitch_modup(c, S, l, dt));
+    return keyswitch_tail(c, S, l, dt, ko);
 }
 
 // rotate a list of physical ciphertexts (each [2][l][n]) by Galois element g
@@ -1401,6 +1412,69 @@ extern "C" int fhe_rotate_multi(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out
         }
     }
     return rotate_phys(c, in, o, l, g);
+}
+
+// Rotations of one ciphertext by m steps sharing one ModUp (Halevi-Shoup hoisting).
+// Per physical ct: digits + ModUp once; per step: the inner product reads the extended
+// digits through the NTT-domain automorphism (Ext(tau_g(c1)) = perm_g(Ext(c1)): the
+// automorphism commutes with the digit lift and permutes NTT slots identically for
+// every prime), then ModDown with tau_g(c0).  Words equal m separate fhe_rotate calls.
+extern "C" int fhe_rotate_hoisted(fhe_ctx *c, const fhe_ct *a, const uint32_t *k, uint32_t m, fhe_ct *const *out) {
+    if (!m) return 0;
+    const u32 l = a->level;
+    std::vector<u32> g(m);
+    for (u32 j = 0; j < m; j++) {
+        TRY(check_rot(c, k[j]));
+        if (!same_shape(a, out[j])) return fail(FHE_ELEVEL, "rotate_hoisted: shape/level mismatch");
+        if (a->d == out[j]->d) return fail(FHE_EINVAL, "rotate_hoisted: out must not alias the input");
+        g[j] = galois_elt(c, k[j]);
+    }
+    const size_t n = c->n, stride = 2ull * l * n;
+    use_lane(c, 0);
+    const int SI = std::max(1, std::min<int>(c->S, (int)a->count));    // source cts per ModUp batch
+    for (u32 b0 = 0; b0 < a->count; b0 += SI) {
+        const int si = (int)std::min<u32>(SI, a->count - b0);
+        // digits of c1 (identity gather) and ModUp, once per source ct
+        PtrTab pt;
+        memset(&pt, 0, sizeof pt);
+        for (int s = 0; s < si; s++) { pt.in[s] = a->d + (b0 + s) * stride; pt.out[s] = nullptr; pt.g[s] = 1; }
+        LOGN_SWITCH(c->logn, launch_row<LG, true>(c, "k_rot_gather_intt", k_rot_gather_intt<LG>, dim3(si, l), c->st,
+                                                  pt, (int)l, c->w_C1, c->w_D, c->d_mods));
+        CHECK_LAUNCH();
+        DigitTab dm;
+        memset(&dm, 0, sizeof dm);
+        for (int s = 0; s < si; s++) dm.coef[s] = c->w_D + (size_t)s * l * n;
+        TRY(keyswitch_modup(c, si, l, dm));
+        // items (source s, step j), at most S per inner-product / ModDown launch
+        const size_t items = (size_t)si * m;
+        for (size_t i0 = 0; i0 < items; i0 += c->S) {
+            const int S = (int)std::min<size_t>(c->S, items - i0);
+            c->key_tick++;
+            DigitTab dt;
+            KsOut ko;
+            memset(&dt, 0, sizeof dt);
+            memset(&ko, 0, sizeof ko);
+            for (int it = 0; it < S; it++) {
+                const size_t item = i0 + it;
+                const u32 j = (u32)(item / si), s = (u32)(item % si);
+                const u64 *src = a->d + (b0 + s) * stride;
+                const u64 *key;
+                TRY(get_key(c, g[j], &key));
+                dt.ntt[it] = src + (size_t)l * n;      // c1 limbs, natural NTT order (diagonal digits)
+                dt.key[it] = key;
+                dt.perm[it] = g[j];
+                dt.esrc[it] = s;
+                ko.out[it] = out[j]->d + (b0 + s) * stride;
+                ko.add[it] = src;                      // c0 limbs, read through the automorphism
+                ko.add_g[it] = g[j];
+            }
+            ko.out_pstride = (long long)l * n;
+            ko.add_pstride = 0;
+            ko.add_pmask = 1;
+            TRY(keyswitch_tail(c, S, l, dt, ko));
+        }
+    }
+    return 0;
 }
 
 extern "C" int fhe_hoisted_dot(fhe_ctx *c, fhe_ct *const *R, const uint32_t *g, uint32_t K, fhe_pt *const *pt,

@@ -190,10 +190,13 @@ struct DigitTab {
     const u64 *coef[MAXS];   // digit j of ct s at coef[s] + j*n (coefficient form, < q_j)
     const u64 *ntt[MAXS];    // the same digits in NTT form (inner-product diagonal)
     const u64 *key[MAXS];    // switching key of ct s (adjacent cts usually share one)
+    u32 perm[MAXS];          // != 0: hoisted rotation -- the extended digits are read through the
+                             // NTT-domain automorphism by this Galois element ...
+    u32 esrc[MAXS];          // ... from Ext block esrc[s] (rotations of one input share its ModUp)
 };
 
-// Key switching, step 2 (ModUp).  grid (S, l, l+1): digit j of ct s reduced into
-// prime i (i == l: the special prime) and transformed; the diagonal i == j is
+// Key switching, step 2 (ModUp).  grid (S, l, l+1): digit j of ct s lifted (centered)
+// into prime i (i == l: the special prime) and transformed; the diagonal i == j is
 // skipped (the inner product reads it from DigitTab.ntt).
 template <int LOGN>
 __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
@@ -204,10 +207,13 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_modup(DigitTab dt, 
     if (i == j) return;
     const long long n = C::N;
     const ModInfo M = mods[i == l ? special_id : i];
+    const ModInfo &Sj = mods[j];
+    const u64 half_j = Sj.half, qj_mod = red64(Sj.q, M.q, M.mu);
     const u64 *src = dt.coef[s] + j * n;
     u64 v[C::E];
+    // centered lift: sign-symmetric, so it commutes with automorphisms (hoisted rotations)
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = red64(src[C::io(tid, e)], M.q, M.mu);
+    for (int e = 0; e < C::E; e++) v[e] = centered_lift(src[C::io(tid, e)], half_j, qj_mod, M);
     ntt_fwd_row<LOGN>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
     for (int x = tid; x < C::NL; x += C::TH) dst[x] = sm[C::pad(x)];
@@ -329,10 +335,13 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
                     ka[j] = __ldg(cur + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
                 }
             }
+            // hoisted rotations share one ModUp: Ext(tau_g(c1)) = Ext(c1) read at perm_g(x)
+            const long long xs = dt.perm[s] ? (long long)galois_perm((u32)x, dt.perm[s], logn) : x;
+            const int es = dt.perm[s] ? (int)dt.esrc[s] : s;
             u64 e[l];
 #pragma unroll
             for (int j = 0; j < l; j++)
-                e[j] = i == j ? dt.ntt[s][(long long)j * n + x] : Ext[((((long long)s * l + j) * (l + 1)) + i) * n + x];
+                e[j] = i == j ? dt.ntt[s][(long long)j * n + xs] : Ext[((((long long)es * l + j) * (l + 1)) + i) * n + xs];
             u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
 #pragma unroll
             for (int j = 0; j < l; j++) {

@@ -161,7 +161,12 @@ class _Hoist:
             step = 1 << (r - 1 - i)
             ks = ks + [k + step for k in ks]
         self.ks = ks
-        rot = _rotate_multi(ctx, [ct] * (len(ks) - 1), ks[1:]) if len(ks) > 1 else []
+        if len(ks) <= 1:
+            rot = []
+        elif hasattr(ctx, "rotate_hoisted"):          # one shared ModUp for all of them
+            rot = ctx.rotate_hoisted(ct, ks[1:])
+        else:
+            rot = _rotate_multi(ctx, [ct] * (len(ks) - 1), ks[1:])
         self.rotated = [ct] + list(rot)
 
 

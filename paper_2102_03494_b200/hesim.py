@@ -597,6 +597,29 @@ class HeContext:
                 outs[i] = self._wrap(h, cts[i].depth, cts[i].assembly_depth)
         return outs
 
+    def rotate_hoisted(self, ct, ks, charge_identity: bool = False):
+        """[rotate(ct, k, charge_identity) for k in ks]: same counters, objects and
+        decrypted slots; the nonzero steps share one digit decomposition + ModUp on
+        the device (fhe_rotate_hoisted), ciphertext words equal separate rotations."""
+        ks = [int(k) for k in ks]
+        n = self.params.n_slots
+        for k in ks:
+            if not 0 <= k < n:
+                raise ValueError(f"rotation amount must be in [0, {n}), got {k}")
+        outs = [ct] * len(ks)
+        for k in ks:
+            if k != 0 or charge_identity:
+                self.counters.rot += 1
+            elif not charge_identity:
+                self.elided_rotations += 1
+        live = sorted({k for k in ks if k != 0})
+        if not live:
+            return outs
+        if not ct.tracked:
+            return [ct if k == 0 else SlotCiphertext(None, ct.depth, ct.params, ct.assembly_depth) for k in ks]
+        hs = dict(zip(live, self.evaluator.rotate_hoisted(ct.handle, live)))
+        return [ct if k == 0 else self._wrap(hs[k], ct.depth, ct.assembly_depth) for k in ks]
+
     def add_cc_many(self, a, b):
         a, b = list(a), list(b)
         self.counters.add_cc += len(a)

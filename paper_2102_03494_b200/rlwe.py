@@ -225,6 +225,13 @@ class Evaluator:
                       handle_array([o.ptr for o in outs]), arr, len(cts))
         return outs
 
+    def rotate_hoisted(self, ct, ks) -> list[Ciphertext]:
+        """rotate(ct, k) for every k, one shared digit decomposition + ModUp."""
+        outs = [self.new_ct(ct.rows, ct.level) for _ in ks]
+        arr = (ctypes.c_uint32 * len(ks))(*[int(k) for k in ks])
+        self.lib.call("fhe_rotate_hoisted", self.ctx, ct.ptr, arr, len(ks), handle_array([o.ptr for o in outs]))
+        return outs
+
     def hoisted_dot(self, R, gs, pts) -> list[Ciphertext]:
         """out[s] = sum_k R[k] * tau_{gs[k]}(pts[s])."""
         outs = [self.new_ct(R[0].rows, R[0].level) for _ in pts]

@@ -191,3 +191,46 @@ def test_lane_reuses_fresh_key_bit_exact(golden_lib, cuda_lib, monkeypatch):
     gp.write(cc, gd.read(cg))
     for k in (1, 12345):
         assert np.array_equal(gd.read(gd.rotate(cg, k)), gp.read(gp.rotate(cc, k))), k
+
+
+def test_pinned_async_encrypt_decrypt_match_sync(golden_lib, cuda_lib):
+    """Page-locked host buffers take the asynchronous copy-stream path (several calls
+    in flight); results equal the synchronous pageable path word for word."""
+    import torch
+    gd, gp, P = _pair(CASES[3], golden_lib, cuda_lib)
+    rng = np.random.default_rng(13)
+    R = 6
+    s = _rand_slots(P, R, rng)
+    pin_in = torch.from_numpy(s.view(np.int64)).pin_memory().numpy().view(np.uint64)
+    pin_out = torch.empty(s.shape, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    cts = [gp.encrypt(pin_in[:, r:r + 2], nonce=100 + r) for r in range(0, R, 2)]
+    rs = gp.rotate_many(cts, 9)
+    for r, c in zip(range(0, R, 2), rs):
+        gp.decrypt(c, out=pin_out[:, r:r + 2])
+    gp.sync()
+    for r, c in zip(range(0, R, 2), cts):
+        ref = gp.encrypt(np.ascontiguousarray(s[:, r:r + 2]), nonce=100 + r)
+        assert np.array_equal(gp.read(ref), gp.read(c))
+    N = P.n_slots
+    A = s
+    exp = np.concatenate([np.roll(A[..., :N], -9, axis=-1), np.roll(A[..., N:], -9, axis=-1)], axis=-1)
+    assert np.array_equal(pin_out, exp)
+
+
+@pytest.mark.parametrize("case", [CASES[2], CASES[4], BIG[1]], ids=lambda c: f"N{c[0]}")
+def test_rotate_hoisted_bit_exact(case, golden_lib, cuda_lib, monkeypatch):
+    """Rotations of one ciphertext sharing one ModUp equal separate golden rotations
+    word for word (several source sub-batches and item chunks at FHE_KS_BATCH=3)."""
+    monkeypatch.setenv("FHE_KS_BATCH", "3")
+    gd, gp, P = _pair(case, golden_lib, cuda_lib)
+    rng = np.random.default_rng(14)
+    R = 2
+    s = _rand_slots(P, R, rng)
+    cg = gd.encrypt(s, nonce=21)
+    cc = gp.new_ct(R)
+    gp.write(cc, gd.read(cg))
+    N = P.n_slots
+    ks = sorted({1, 2, N // 2 - 1, N - 1, int(rng.integers(1, N))})
+    outs = gp.rotate_hoisted(cc, ks)
+    for k, o in zip(ks, outs):
+        assert np.array_equal(gd.read(gd.rotate(cg, k)), gp.read(o)), k

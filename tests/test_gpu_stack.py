@@ -96,3 +96,23 @@ def test_cfg0_hoisted_on_gpu(cuda_lib):
         assert [str(int(v)) for v in row] == want
     assert res.counters.rot < 4889 // 2
     assert min(ctx.noise_budget(ct) for ct in res.value.cts) > 5
+
+
+def test_h_im2col_moves_hoisted_on_gpu(cuda_lib, golden_lib):
+    """H-Im2Col moves (packing.py:249-279) with every rotation of one masked source
+    sharing one ModUp: plaintext im2col, the reference's counts, golden words."""
+    from paper_2102_03494_b200.packing import (ChannelPacked, KernelSpec, conv_unpack, dense_pack,
+                                               h_im2col_from_conv, h_im2col_from_dense, plain_im2col)
+    rng = np.random.default_rng(31)
+    x = rng.integers(-5, 6, size=(2, 3, 5, 5))
+    k = KernelSpec(d=2, stride=1, out_channels=1)
+    words = []
+    for lib in (cuda_lib, golden_lib):
+        sch = scheme_from(128, [65537], levels=4)
+        ctx = HeContext(sch, batch=2, lib=lib)
+        cols = h_im2col_from_dense(dense_pack(x, ctx), k, ctx)
+        assert np.array_equal(conv_unpack(cols, ctx).astype(np.int64), plain_im2col(x, k))
+        assert ctx.counters.rot == ctx.counters.add_cc == 16 * 12
+        words.append([ctx.evaluator.read(c.handle) for c in cols.cts])
+    for a, b in zip(*words):
+        assert np.array_equal(a, b)
