@@ -84,6 +84,9 @@ int fhe_ctx_stream(fhe_ctx *ctx, void **stream);
 /* measured integer-pipe roofline: chained 64-bit Shoup modular multiplications
  * per second over the whole GPU (register resident, all SMs) */
 int fhe_peak_modmul(fhe_ctx *ctx, uint32_t iters, double *modmul_per_s);
+/* kind 0: exact-quotient Shoup chains (= fhe_peak_modmul); kind 1: the
+ * approximate-quotient Shoup form the NTT butterflies issue. */
+int fhe_peak_modmul_kind(fhe_ctx *ctx, uint32_t iters, int kind, double *modmul_per_s);
 /* per-kernel CUDA-event profiling: when enabled, every launch is bracketed by
  * events; fhe_prof_report syncs and writes "name calls total_ms\n" lines
  * (then clears).  fhe_launch_count: kernels launched since creation. */

@@ -529,6 +529,10 @@ int fhe_peak_modmul(fhe_ctx *ctx, uint32_t iters, double *out) {
     (void)ctx; (void)iters; *out = 0.0;
     return fail(FHE_EINVAL, "no device in the golden model");
 }
+int fhe_peak_modmul_kind(fhe_ctx *ctx, uint32_t iters, int kind, double *out) {
+    (void)kind;
+    return fhe_peak_modmul(ctx, iters, out);
+}
 int fhe_ctx_key_bytes(fhe_ctx *ctx, uint64_t *out) { *out = ctx->key_bytes; return 0; }
 
 /* ------------------------------------------------------------------ */

@@ -20,7 +20,8 @@ FHE_MAX_B = 26
 FHE_MAX_T = 8
 
 PACKAGE_DIR = os.path.dirname(os.path.abspath(__file__))
-CUDA_LIB_PATH = os.path.join(PACKAGE_DIR, "_lib", "libffconv_he.so")
+# FFCONV_HE_LIB: an alternative in-tree build of the same library (experiment variants)
+CUDA_LIB_PATH = os.environ.get("FFCONV_HE_LIB") or os.path.join(PACKAGE_DIR, "_lib", "libffconv_he.so")
 
 
 class FheParams(ctypes.Structure):
@@ -54,6 +55,7 @@ SIGNATURES = {
     "fhe_keygen_rotations": (c_int, [c_void_p, POINTER(c_uint32), c_uint32]),
     "fhe_ctx_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "fhe_peak_modmul": (c_int, [c_void_p, c_uint32, POINTER(c_double)]),
+    "fhe_peak_modmul_kind": (c_int, [c_void_p, c_uint32, c_int, POINTER(c_double)]),
     "fhe_prof_enable": (c_int, [c_void_p, c_int]),
     "fhe_prof_report": (c_int, [c_void_p, ctypes.c_char_p, c_uint32]),
     "fhe_launch_count": (c_int, [c_void_p, _U64P]),

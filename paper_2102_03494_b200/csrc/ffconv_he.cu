@@ -486,6 +486,8 @@ static int setup_moduli(fhe_ctx *c) {
         M.ninv = hm::inv(n, q);
         M.ninv_sh = hm::shoup(M.ninv, q);
         M.half = (q - 1) / 2;
+        M.nq = (u64)0 - q;
+        M.q3 = 3 * q;
         u64 *dbase = c->d_tw + (size_t)id * 4 * n;
         M.tw = (const ulonglong2 *)dbase;
         M.itw = (const ulonglong2 *)(dbase + 2 * n);
@@ -694,7 +696,9 @@ extern "C" int fhe_ctx_stream(fhe_ctx *c, void **stream) {
     return 0;
 }
 
-extern "C" int fhe_peak_modmul(fhe_ctx *c, uint32_t iters, double *out) {
+extern "C" int fhe_peak_modmul_kind(fhe_ctx *c, uint32_t iters, int kind, double *out) {
+    if (kind != 0 && kind != 1) return fail(FHE_EINVAL, "peak kind must be 0 (exact Shoup) or 1 (approximate-quotient Shoup)");
+    auto kern = kind ? k_peak_modmul<1> : k_peak_modmul<0>;
     int sms = 0;
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev));
     const int blocks = sms * 8, threads = 256;
@@ -704,9 +708,9 @@ extern "C" int fhe_peak_modmul(fhe_ctx *c, uint32_t iters, double *out) {
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
-    k_peak_modmul<<<blocks, threads, 0, c->st>>>(sink, iters / 8 + 1, q, w, wsh);   // warm-up
+    kern<<<blocks, threads, 0, c->st>>>(sink, iters / 8 + 1, q, w, wsh);   // warm-up
     CU(cudaEventRecord(e0, c->st));
-    k_peak_modmul<<<blocks, threads, 0, c->st>>>(sink, iters, q, w, wsh);
+    kern<<<blocks, threads, 0, c->st>>>(sink, iters, q, w, wsh);
     CU(cudaEventRecord(e1, c->st));
     CU(cudaEventSynchronize(e1));
     float ms = 0;
@@ -717,6 +721,7 @@ extern "C" int fhe_peak_modmul(fhe_ctx *c, uint32_t iters, double *out) {
     *out = (double)blocks * threads * 8.0 * iters / (ms * 1e-3);
     return 0;
 }
+extern "C" int fhe_peak_modmul(fhe_ctx *c, uint32_t iters, double *out) { return fhe_peak_modmul_kind(c, iters, 0, out); }
 
 extern "C" int fhe_prof_enable(fhe_ctx *c, int on) {
     c->prof = on != 0;

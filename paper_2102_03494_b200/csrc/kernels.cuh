@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_ntt_rows(NttRowsArg
 #pragma unroll
     for (int e = 0; e < C::E; e++) {
         u64 x = src[C::io(tid, e)];
-        if (a.load == 1) x = red64(x, M.q, M.mu);
-        else if (a.load == 2) x = centered_lift(x, half_src, msrc_q, M);
+        if (a.load == 1) x = red_lazy(x, M);
+        else if (a.load == 2) x = centered_lift_lazy(x, half_src, msrc_q, M);
         v[e] = x;
     }
     ntt_fwd_row<LOGN>(v, sm, M, tid);
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_modup(DigitTab dt, 
     u64 v[C::E];
     // centered lift: sign-symmetric, so it commutes with automorphisms (hoisted rotations)
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = centered_lift(src[C::io(tid, e)], half_j, qj_mod, M);
+    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(src[C::io(tid, e)], half_j, qj_mod, M);
     ntt_fwd_row<LOGN>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
     for (int x = tid; x < C::NL; x += C::TH) dst[x] = sm[C::pad(x)];
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_rescale(RescaleArgs
     const u64 *r = a.coef[s] + p * a.coef_pstride;
     u64 v[C::E];
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = centered_lift(r[C::io(tid, e)], half_src, msrc_q, M);
+    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(r[C::io(tid, e)], half_src, msrc_q, M);
     ntt_fwd_row<LOGN>(v, sm, M, tid);
     const u64 *base = a.base[s] + p * a.base_pstride + i * n + gb;
     u64 *out = a.out[s] + p * a.out_pstride + i * n + gb;
@@ -701,14 +701,18 @@ __global__ void k_from_mont(const u64 *__restrict__ in, u64 *__restrict__ out, l
 }
 
 // integer-pipe roofline probe: 8 independent chains of lazy Shoup modmuls per
-// thread, register resident; counts 8 * iters modmuls per thread.
+// thread, register resident; counts 8 * iters modmuls per thread.  APPROX = 0:
+// exact quotient (shoup_lazy); APPROX = 1: the approximate-quotient form the NTT
+// butterflies use (shoup_approx), i.e. the fastest modmul this library issues.
+template <int APPROX>
 __global__ void k_peak_modmul(u64 *sink, u32 iters, u64 q, u64 w, u64 wsh) {
     u64 x[8];
+    const u64 nq = (u64)0 - q;
 #pragma unroll
     for (int k = 0; k < 8; k++) x[k] = threadIdx.x * 8 + k + blockIdx.x;
     for (u32 it = 0; it < iters; it++) {
 #pragma unroll
-        for (int k = 0; k < 8; k++) x[k] = shoup_lazy(x[k], w, wsh, q);
+        for (int k = 0; k < 8; k++) x[k] = APPROX ? shoup_approx(x[k], w, wsh, nq) : shoup_lazy(x[k], w, wsh, q);
     }
     u64 acc = 0;
 #pragma unroll

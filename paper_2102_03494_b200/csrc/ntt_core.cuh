@@ -16,6 +16,58 @@
 #pragma once
 #include "arith.cuh"
 
+// Lazy-reduction schedule.  Butterfly values are bounded, not reduced: with
+// LIM = 2^clz(q) (so LIM q < 2^64), a forward (Cooley-Tukey) stage adds < 3q to
+// every value (approximate-quotient Shoup products lie in [0, 3q)) and the U
+// operands are conditionally reduced by (LIM/2) q only in the stages where the
+// bound would pass LIM q; an inverse (Gentleman-Sande) stage doubles the bound of
+// the sums, which are conditionally reduced once it reaches LIM/2.  Bounds are
+// tracked in units of q, uniformly over the CTA, so the reduction choice is a
+// uniform branch per stage.  A forward NTT never reduces for q < 2^58; neither
+// does an inverse one for the 40-bit primes of configs[1].  The outputs are
+// canonical, hence bit-identical to the exact butterflies of the golden model.
+struct FwdLazy {
+    u64 nq, q3, cq;
+    int lim, B;          // LIM, and the current bound of every value (units of q)
+    bool red;            // this stage reduces its U operands by cq
+    DEV explicit FwdLazy(const ModInfo &M) : nq(M.nq), q3(M.q3), B(4), red(false) {
+        const int z = min(__clzll(M.q), 24);
+        lim = 1 << z;
+        cq = M.q << (z - 1);
+    }
+    // inputs < 4q; call once per stage, before its butterflies
+    DEV void stage() {
+        red = B + 3 > lim;
+        B = red ? max(lim >> 1, B - (lim >> 1)) + 3 : B + 3;
+    }
+    DEV u64 cred(u64 u) const { return u >= cq ? u - cq : u; }
+    DEV void bfly(u64 &a, u64 &b, const ulonglong2 &tw) const {
+        const u64 U = a, V = shoup_approx(b, tw.x, tw.y, nq);
+        a = U + V;
+        b = U - V + q3;
+    }
+};
+struct InvLazy {
+    u64 q, nq, Bq;       // Bq = (input bound) * q
+    int lgB, sB;         // log2 of the largest bound, log2 of the current bound
+    bool red;            // this stage reduces its sums by Bq
+    DEV explicit InvLazy(const ModInfo &M) : q(M.q), nq(M.nq), Bq(2 * M.q), sB(1), red(false) {
+        lgB = min(__clzll(M.q), 24) - 1;
+    }
+    // inputs < 2q; call once per stage, before its butterflies
+    DEV void stage() {
+        Bq = q << sB;
+        red = sB + 1 > lgB;
+        if (!red) sB++;
+    }
+    DEV u64 cred(u64 s) const { return s >= Bq ? s - Bq : s; }
+    DEV void bfly(u64 &a, u64 &b, const ulonglong2 &tw) const {
+        const u64 U = a, V = b;
+        a = U + V;
+        b = shoup_approx(U - V + Bq, tw.x, tw.y, nq);
+    }
+};
+
 #ifndef NTT_W_FWD
 #define NTT_W_FWD 4
 #endif
@@ -63,7 +115,7 @@ template <int LOGN, int WW = DefaultW<LOGN>::value>
 DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid) {
     using C = NttCfg<LOGN, WW>;
     constexpr int W = C::W, E = C::E, NP = C::NP;
-    const u64 q = M.q, q2 = 2 * q;
+    FwdLazy Lz(M);
 #pragma unroll
     for (int p = 0; p < NP; p++) {
         const int s0 = p * W;
@@ -78,27 +130,23 @@ DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
         for (int ls = 0; ls < k; ls++) {
             const int s = s0 + ls;
             const int b = LOGN - s - 1 - f0;
+            Lz.stage();
+            if (Lz.red) {
+#pragma unroll
+                for (int e = 0; e < E; e++)
+                    if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
+            }
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
                 const int e2 = e | (1 << b);
                 const u32 g = (1u << s) + ((u32)fidx<W>(tid, e, f0) >> (LOGN - s));
-                const ulonglong2 tw = __ldg(M.tw + g);
-                const u64 w = tw.x, wsh = tw.y;
-                u64 U = v[e];
-                U = U >= q2 ? U - q2 : U;
-                u64 V = shoup_lazy(v[e2], w, wsh, q);
-                v[e] = U + V;
-                v[e2] = U - V + q2;
+                Lz.bfly(v[e], v[e2], __ldg(M.tw + g));
             }
         }
         if (p == NP - 1) {
 #pragma unroll
-            for (int e = 0; e < E; e++) {
-                u64 x = v[e];
-                x = x >= q2 ? x - q2 : x;
-                v[e] = x >= q ? x - q : x;
-            }
+            for (int e = 0; e < E; e++) v[e] = red_any(v[e], M.q, M.mu, M.nq);
         }
 #pragma unroll
         for (int e = 0; e < E; e++) sm[C::pad(fidx<W>(tid, e, f0))] = v[e];
@@ -113,7 +161,8 @@ template <int LOGN, int WW = DefaultWInv<LOGN>::value>
 DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid, u32 g_perm = 0) {
     using C = NttCfg<LOGN, WW>;
     constexpr int W = C::W, E = C::E, NP = C::NP, N = C::N;
-    const u64 q = M.q, q2 = 2 * q;
+    const u64 q = M.q;
+    InvLazy Lz(M);
 #pragma unroll
     for (int p = 0; p < NP; p++) {
         const int lt0 = p * W;                                   // log2 t of the first stage
@@ -132,17 +181,18 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
             const int lt = lt0 + ls;
             const int b = lt - f0;
             const int h = N >> (lt + 1);
+            Lz.stage();
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
                 const int e2 = e | (1 << b);
                 const u32 g = (u32)h + ((u32)fidx<W>(tid, e, f0) >> (lt + 1));
-                const ulonglong2 tw = __ldg(M.itw + g);
-                const u64 w = tw.x, wsh = tw.y;
-                u64 U = v[e], V = v[e2];
-                u64 s = U + V;
-                v[e] = s >= q2 ? s - q2 : s;
-                v[e2] = shoup_lazy(U - V + q2, w, wsh, q);
+                Lz.bfly(v[e], v[e2], __ldg(M.itw + g));
+            }
+            if (Lz.red) {
+#pragma unroll
+                for (int e = 0; e < E; e++)
+                    if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
             }
         }
         if (p < NP - 1) {
@@ -169,9 +219,12 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
 // golden model.  For n <= 2^14 RowCfg is the single-CTA configuration (CR = 1).
 #include <cooperative_groups.h>
 
+#ifndef NTT_LOGL
+#define NTT_LOGL 14      // rows up to 2^NTT_LOGL words run on one CTA
+#endif
 template <int LOGN, bool INV>
 struct RowCfg {
-    static constexpr int LOGL = LOGN > 14 ? 14 : LOGN;    // log2 words per CTA
+    static constexpr int LOGL = LOGN > 14 ? 14 : (LOGN > NTT_LOGL ? NTT_LOGL : LOGN);    // log2 words per CTA
     static constexpr int CL = LOGN - LOGL;                // log2 CTAs per row
     static constexpr int CR = 1 << CL;
     using Loc = NttCfg<LOGL, INV ? DefaultWInv<LOGL>::value : DefaultW<LOGL>::value>;
@@ -194,23 +247,24 @@ DEV void ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInf
     namespace cg = cooperative_groups;
     using R = RowCfg<LOGN, false>;
     constexpr int W = R::W, E = R::E, LOGL = R::LOGL, CL = R::CL;
-    const u64 q = M.q, q2 = 2 * q;
+    FwdLazy Lz(M);
     const int rank = R::rank(), gtid = rank * R::TH + tid;
     cg::cluster_group cl = cg::this_cluster();
     // stages 0 .. W-1: the pair partner differs in bit W-1-s of e
 #pragma unroll
     for (int s = 0; s < W; s++) {
         const int b = W - 1 - s;
+        Lz.stage();
+        if (Lz.red) {
+#pragma unroll
+            for (int e = 0; e < E; e++)
+                if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
+        }
 #pragma unroll
         for (int e = 0; e < E; e++) {
             if (e & (1 << b)) continue;
             const int e2 = e | (1 << b);
-            const ulonglong2 tw = __ldg(M.tw + (1 << s) + (e >> (W - s)));
-            u64 U = v[e];
-            U = U >= q2 ? U - q2 : U;
-            const u64 V = shoup_lazy(v[e2], tw.x, tw.y, q);
-            v[e] = U + V;
-            v[e2] = U - V + q2;
+            Lz.bfly(v[e], v[e2], __ldg(M.tw + (1 << s) + (e >> (W - s))));
         }
     }
     cl.sync();   // every CTA of the cluster is resident before remote stores
@@ -237,26 +291,23 @@ DEV void ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInf
         for (int ls = 0; ls < k; ls++) {
             const int sl = s0 + ls;
             const int b = LOGL - sl - 1 - f0;
+            Lz.stage();
+            if (Lz.red) {
+#pragma unroll
+                for (int e = 0; e < E; e++)
+                    if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
+            }
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
                 const int e2 = e | (1 << b);
                 const u32 g = (1u << (sl + CL)) + ((u32)rank << sl) + ((u32)fidx<W>(tid, e, f0) >> (LOGL - sl));
-                const ulonglong2 tw = __ldg(M.tw + g);
-                u64 U = v[e];
-                U = U >= q2 ? U - q2 : U;
-                const u64 V = shoup_lazy(v[e2], tw.x, tw.y, q);
-                v[e] = U + V;
-                v[e2] = U - V + q2;
+                Lz.bfly(v[e], v[e2], __ldg(M.tw + g));
             }
         }
         if (p == NP - 1) {
 #pragma unroll
-            for (int e = 0; e < E; e++) {
-                u64 x = v[e];
-                x = x >= q2 ? x - q2 : x;
-                v[e] = x >= q ? x - q : x;
-            }
+            for (int e = 0; e < E; e++) v[e] = red_any(v[e], M.q, M.mu, M.nq);
         }
 #pragma unroll
         for (int e = 0; e < E; e++) sm[R::pad(fidx<W>(tid, e, f0))] = v[e];
@@ -271,7 +322,8 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
     namespace cg = cooperative_groups;
     using R = RowCfg<LOGN, true>;
     constexpr int W = R::W, E = R::E, LOGL = R::LOGL, CL = R::CL, N = R::N;
-    const u64 q = M.q, q2 = 2 * q;
+    const u64 q = M.q;
+    InvLazy Lz(M);
     const int rank = R::rank(), gtid = rank * R::TH + tid;
     cg::cluster_group cl = cg::this_cluster();
     constexpr int LT = LOGL - W + CL;            // local stages lt = 0 .. LT-1
@@ -288,16 +340,18 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
         for (int ls = 0; ls < k; ls++) {
             const int lt = lt0 + ls;
             const int b = lt - f0;
+            Lz.stage();
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
                 const int e2 = e | (1 << b);
                 const u32 g = (u32)(N >> (lt + 1)) + ((u32)rank << (LOGL - lt - 1)) + ((u32)fidx<W>(tid, e, f0) >> (lt + 1));
-                const ulonglong2 tw = __ldg(M.itw + g);
-                const u64 U = v[e], V = v[e2];
-                const u64 s = U + V;
-                v[e] = s >= q2 ? s - q2 : s;
-                v[e2] = shoup_lazy(U - V + q2, tw.x, tw.y, q);
+                Lz.bfly(v[e], v[e2], __ldg(M.itw + g));
+            }
+            if (Lz.red) {
+#pragma unroll
+                for (int e = 0; e < E; e++)
+                    if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
             }
         }
 #pragma unroll
@@ -316,15 +370,17 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
 #pragma unroll
     for (int b = 0; b < W; b++) {
         const int lt = LOGN - W + b;
+        Lz.stage();
 #pragma unroll
         for (int e = 0; e < E; e++) {
             if (e & (1 << b)) continue;
             const int e2 = e | (1 << b);
-            const ulonglong2 tw = __ldg(M.itw + (N >> (lt + 1)) + (e >> (b + 1)));
-            const u64 U = v[e], V = v[e2];
-            const u64 s = U + V;
-            v[e] = s >= q2 ? s - q2 : s;
-            v[e2] = shoup_lazy(U - V + q2, tw.x, tw.y, q);
+            Lz.bfly(v[e], v[e2], __ldg(M.itw + (N >> (lt + 1)) + (e >> (b + 1))));
+        }
+        if (Lz.red) {
+#pragma unroll
+            for (int e = 0; e < E; e++)
+                if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
         }
     }
     cl.sync();   // no CTA leaves or reuses its shared memory while another reads it
