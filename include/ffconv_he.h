@@ -93,6 +93,10 @@ int fhe_peak_modmul_kind(fhe_ctx *ctx, uint32_t iters, int kind, double *modmul_
 int fhe_prof_enable(fhe_ctx *ctx, int on);
 int fhe_prof_report(fhe_ctx *ctx, char *buf, uint32_t len);
 int fhe_launch_count(fhe_ctx *ctx, uint64_t *out);
+/* algorithmic modular multiplications issued since creation: (n/2) log2 n per
+ * row (I)NTT, 2 l (l+1) n + 2 l n per key switch (inner product + ModDown
+ * scaling), 2 l n per hoisted-dot term; elementwise ops are not counted. */
+int fhe_work_modmuls(fhe_ctx *ctx, double *out);
 /* development diagnostic: time `iters` launches of an n-point (inverse) NTT over
  * `rows` rows of modulus q_0 with a radix-2^W register core (W in {3,4,5,6});
  * *ms = average launch time, *mismatch = rows whose output differs from W = 4 */

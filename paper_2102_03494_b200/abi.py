@@ -56,6 +56,7 @@ SIGNATURES = {
     "fhe_ctx_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "fhe_peak_modmul": (c_int, [c_void_p, c_uint32, POINTER(c_double)]),
     "fhe_peak_modmul_kind": (c_int, [c_void_p, c_uint32, c_int, POINTER(c_double)]),
+    "fhe_work_modmuls": (c_int, [c_void_p, POINTER(c_double)]),
     "fhe_prof_enable": (c_int, [c_void_p, c_int]),
     "fhe_prof_report": (c_int, [c_void_p, ctypes.c_char_p, c_uint32]),
     "fhe_launch_count": (c_int, [c_void_p, _U64P]),

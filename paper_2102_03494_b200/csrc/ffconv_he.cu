@@ -173,6 +173,7 @@ struct fhe_ctx {
     // profiling
     bool prof = false;
     u64 launches = 0;
+    double alg_mm = 0;                  // algorithmic modmuls issued (fhe_work_modmuls)
     struct Rec { const char *name; cudaEvent_t a, b; };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> ev_pool;
@@ -242,6 +243,7 @@ static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim
     ProfScope ps_(c, name);
     using C = RowCfg<LOGN, INV>;
     const size_t smem = (size_t)C::SMEM_WORDS * sizeof(u64);
+    c->alg_mm += (double)grid.x * grid.y * grid.z * (C::N / 2) * LOGN;      // one (I)NTT per row
     {
         std::lock_guard<std::mutex> lk(g_attr_mu);
         if (!g_attr_done.count((const void *)kern)) {
@@ -849,6 +851,11 @@ extern "C" int fhe_bench_ntt(fhe_ctx *c, int W, int inverse, uint32_t rows, uint
     return rc;
 }
 
+extern "C" int fhe_work_modmuls(fhe_ctx *c, double *out) {
+    *out = c->alg_mm;
+    return 0;
+}
+
 extern "C" int fhe_launch_count(fhe_ctx *c, uint64_t *out) {
     *out = c->launches;
     return 0;
@@ -1217,6 +1224,7 @@ struct KsOut {
 
 // ModUp: every off-diagonal (digit, prime) pair of S cts into Ext
 static int keyswitch_modup(fhe_ctx *c, int S, u32 l, const DigitTab &dt) {
+    c->alg_mm -= (double)S * l * (c->n / 2) * c->logn;      // the diagonal rows return at once
     LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_modup", k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
                                         c->d_mods));
     CHECK_LAUNCH();
@@ -1232,6 +1240,7 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     static int ksv = -1;
     if (ksv < 0) { const char *e = getenv("FHE_KS_VARIANT"); ksv = e ? atoi(e) : 2; }   // 2: measured best (4 cts/thread, 4 CTAs/SM)
     const int G = (ksv == 1 || ksv == 3) ? 2 : 4;
+    c->alg_mm += (double)S * (2.0 * l * (l + 1) + 2.0 * l) * n;   // key inner product + ModDown scaling
     long long tot = (long long)((S + G - 1) / G) * (l + 1) * n;
     {
         ProfScope ps_(c, "k_ks_inner");
@@ -1502,6 +1511,7 @@ extern "C" int fhe_hoisted_dot(fhe_ctx *c, fhe_ct *const *R, const uint32_t *g, 
         a.K = (int)K; a.S = (int)St; a.Rr = (int)R[0]->R; a.l = (int)l; a.L = (int)c->L; a.logn = (int)c->logn;
         dim3 grid((unsigned)(c->n / 32 > 0 ? c->n / 32 : 1), c->T * l, (St + 7) / 8);
         if (c->n < 32) return fail(FHE_EINVAL, "hoisted_dot needs n >= 32");
+        c->alg_mm += (double)St * K * c->T * R[0]->R * 2.0 * l * c->n;
         ProfScope ps_(c, "k_hoisted_dot");
         k_hoisted_dot<<<grid, 256, 0, c->st>>>(a, c->d_mods);
         CHECK_LAUNCH();

@@ -214,9 +214,15 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_modup(DigitTab dt, 
     // centered lift: sign-symmetric, so it commutes with automorphisms (hoisted rotations)
 #pragma unroll
     for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(src[C::io(tid, e)], half_j, qj_mod, M);
-    ntt_fwd_row<LOGN>(v, sm, M, tid);
+    const int B = ntt_fwd_row<LOGN, false>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
-    for (int x = tid; x < C::NL; x += C::TH) dst[x] = sm[C::pad(x)];
+    // the inner product accepts lazy digits while l * B * q < 2^64 (128-bit sums stay
+    // below q 2^64, the Montgomery reduction's input bound)
+    if ((u128)l * (u64)B * M.q < ((u128)1 << 64)) {
+        for (int x = tid; x < C::NL; x += C::TH) dst[x] = sm[C::pad(x)];
+    } else {
+        for (int x = tid; x < C::NL; x += C::TH) dst[x] = red_any(sm[C::pad(x)], M.q, M.mu, M.nq);
+    }
 }
 
 // Rescale by a dropped prime (ModDown over the special prime, or BFV modulus
@@ -250,16 +256,26 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_rescale(RescaleArgs
     u64 v[C::E];
 #pragma unroll
     for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(r[C::io(tid, e)], half_src, msrc_q, M);
-    ntt_fwd_row<LOGN>(v, sm, M, tid);
+    const int B = ntt_fwd_row<LOGN, false>(v, sm, M, tid);
     const u64 *base = a.base[s] + p * a.base_pstride + i * n + gb;
     u64 *out = a.out[s] + p * a.out_pstride + i * n + gb;
     const u64 *add = ((a.add_pmask >> p) & 1) && a.add[s] ? a.add[s] + p * a.add_pstride + i * n : nullptr;
     const u64 f = a.fac[i], fsh = a.fac_sh[i];
     u64 y[C::E];
+    if ((u128)(B + 1) * M.q < ((u128)1 << 64)) {
+        // lazy NTT outputs x < B q: base - x == base + B q - x (mod q), non-negative, < 2^64
+        const u64 Bq = (u64)B * M.q;
 #pragma unroll
-    for (int e = 0; e < C::E; e++) {
-        const int x = tid + e * C::TH;
-        y[e] = shoup(subm(base[x], sm[C::pad(x)], M.q), f, fsh, M.q);
+        for (int e = 0; e < C::E; e++) {
+            const int x = tid + e * C::TH;
+            y[e] = shoup(base[x] + Bq - sm[C::pad(x)], f, fsh, M.q);
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < C::E; e++) {
+            const int x = tid + e * C::TH;
+            y[e] = shoup(subm(base[x], red_any(sm[C::pad(x)], M.q, M.mu, M.nq), M.q), f, fsh, M.q);
+        }
     }
     const u32 add_g = a.add_g[s];
     if (add && add_g) {

@@ -111,8 +111,10 @@ DEV int fidx(int tid, int e, int f0) {
 // Forward. In: v[] holds element fidx(tid, e, LOGN - W) (i.e. v[e] = a[(e << (LOGN-W)) | tid])
 // with values < 4q.  Out: canonical values in sm[C::pad(i)], bit-reversed order; ends
 // with __syncthreads().
-template <int LOGN, int WW = DefaultW<LOGN>::value>
-DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid) {
+// CANON = false: the outputs are left lazy; the return value is their bound in
+// units of q (every output < bound * q <= 2^64), for callers that absorb it.
+template <int LOGN, int WW = DefaultW<LOGN>::value, bool CANON = true>
+DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid) {
     using C = NttCfg<LOGN, WW>;
     constexpr int W = C::W, E = C::E, NP = C::NP;
     FwdLazy Lz(M);
@@ -144,7 +146,7 @@ DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
                 Lz.bfly(v[e], v[e2], __ldg(M.tw + g));
             }
         }
-        if (p == NP - 1) {
+        if (CANON && p == NP - 1) {
 #pragma unroll
             for (int e = 0; e < E; e++) v[e] = red_any(v[e], M.q, M.mu, M.nq);
         }
@@ -152,6 +154,7 @@ DEV void ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
         for (int e = 0; e < E; e++) sm[C::pad(fidx<W>(tid, e, f0))] = v[e];
         __syncthreads();
     }
+    return CANON ? 1 : Lz.B;
 }
 
 // Inverse. In: canonical (or < 2q) values in sm[C::pad(i)], bit-reversed order, synced.
@@ -242,8 +245,8 @@ struct RowCfg {
     static DEV int io(int tid, int e) { return (e << (LOGN - W)) | (rank() * TH + tid); }
 };
 
-template <int LOGN>
-DEV void ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo &M, int tid) {
+template <int LOGN, bool CANON = true>
+DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo &M, int tid) {
     namespace cg = cooperative_groups;
     using R = RowCfg<LOGN, false>;
     constexpr int W = R::W, E = R::E, LOGL = R::LOGL, CL = R::CL;
@@ -305,7 +308,7 @@ DEV void ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInf
                 Lz.bfly(v[e], v[e2], __ldg(M.tw + g));
             }
         }
-        if (p == NP - 1) {
+        if (CANON && p == NP - 1) {
 #pragma unroll
             for (int e = 0; e < E; e++) v[e] = red_any(v[e], M.q, M.mu, M.nq);
         }
@@ -313,6 +316,7 @@ DEV void ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInf
         for (int e = 0; e < E; e++) sm[R::pad(fidx<W>(tid, e, f0))] = v[e];
         __syncthreads();
     }
+    return CANON ? 1 : Lz.B;
 }
 
 // In: this CTA's words (global base() + x) canonical in sm[pad(x)], synced.
@@ -389,10 +393,10 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
 }
 
 // Row-size dispatch used by the row kernels.
-template <int LOGN>
-DEV void ntt_fwd_row(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo &M, int tid) {
-    if constexpr (RowCfg<LOGN, false>::CL == 0) ntt_fwd_core<LOGN>(v, sm, M, tid);
-    else ntt_fwd_cluster<LOGN>(v, sm, M, tid);
+template <int LOGN, bool CANON = true>
+DEV int ntt_fwd_row(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo &M, int tid) {
+    if constexpr (RowCfg<LOGN, false>::CL == 0) return ntt_fwd_core<LOGN, DefaultW<LOGN>::value, CANON>(v, sm, M, tid);
+    else return ntt_fwd_cluster<LOGN, CANON>(v, sm, M, tid);
 }
 template <int LOGN>
 DEV void ntt_inv_row(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo &M, int tid) {
