@@ -55,3 +55,15 @@ for ch in (8,):
         for (r0, r1), r in zip(bounds, rs):
             ev.decrypt(r, out=pin_out[:, r0:r1])
     t(f"e2e enc/dec chunks={ch} + rotate_many", step2)
+
+# per-kernel breakdown of encrypt / decrypt (single stream, isolated kernel times)
+import ctypes  # noqa: E402
+lib = ev.lib
+for label, fn in (("encrypt", lambda: ev.encrypt(pin_in)), ("decrypt", lambda: ev.decrypt(ct, out=pin_out))):
+    fn(); ev.sync()
+    lib.call("fhe_prof_enable", ev.ctx, 1)
+    fn(); ev.sync()
+    buf = ctypes.create_string_buffer(1 << 16)
+    lib.call("fhe_prof_report", ev.ctx, buf, len(buf))
+    lib.call("fhe_prof_enable", ev.ctx, 0)
+    print(label, buf.value.decode().strip().replace("\n", " | "))
