@@ -137,6 +137,7 @@ struct fhe_ctx {
     AuxDev *d_ax = nullptr;
     u64 *d_pmod = nullptr;             // P mod prime_i, i in [0, L]
     u64 pinv[MAXQ]{}, pinv_sh[MAXQ]{};
+    u64 pmont[MAXQ]{};                  // P * 2^64 mod q_i (key-switch addends, KsAdd)
     std::unordered_map<u32, KeyBuf> keys;
     u64 key_bytes = 0;
     // Keys are regenerated deterministically (seed, Galois element), so the store is a
@@ -526,6 +527,7 @@ static int setup_secret(fhe_ctx *c) {
     for (u32 i = 0; i < c->L; i++) {
         c->pinv[i] = hm::inv(pm[i], c->P.q[i]);
         c->pinv_sh[i] = hm::shoup(c->pinv[i], c->P.q[i]);
+        c->pmont[i] = hm::mont(pm[i], c->P.q[i]);
     }
     CU(cudaMalloc((void **)&c->d_pmod, (c->L + 1) * 8));
     CU(cudaMemcpy(c->d_pmod, pm.data(), (c->L + 1) * 8, cudaMemcpyHostToDevice));
@@ -1242,11 +1244,26 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     const int G = (ksv == 1 || ksv == 3) ? 2 : 4;
     c->alg_mm += (double)S * (2.0 * l * (l + 1) + 2.0 * l) * n;   // key inner product + ModDown scaling
     long long tot = (long long)((S + G - 1) / G) * (l + 1) * n;
+    // fold the addends into the inner product while its Montgomery input bound holds
+    // ((l + 2) q_i < 2^64: l digit terms + 2 addend terms, each < q_i^2); else the
+    // rescale epilogue adds them
+    u64 maxq = 0;
+    for (u32 i = 0; i < l; i++) maxq = std::max<u64>(maxq, c->P.q[i]);
+    const bool fold = (u128)(l + 2) * maxq < ((u128)1 << 64);
+    KsAdd kad;
+    memset(&kad, 0, sizeof kad);
+    if (fold) {
+        for (int s = 0; s < S; s++) { kad.add[s] = ko.add[s]; kad.add_g[s] = ko.add_g[s]; kad.acc[s] = ko.acc[s]; }
+        kad.add_pstride = ko.add_pstride;
+        kad.acc_pstride = ko.acc_pstride;
+        kad.add_pmask = ko.add_pmask;
+        for (u32 i = 0; i < l; i++) kad.pr[i] = c->pmont[i];
+    }
     {
         ProfScope ps_(c, "k_ks_inner");
         const unsigned nb = (unsigned)nblocks(tot);
 #define KS_LAUNCH(LLV, GV, MB) k_ks_inner<LLV, GV, MB><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, \
-                                                        (int)c->logn, c->special_id, c->d_mods)
+                                                        (int)c->logn, c->special_id, c->d_mods, kad)
 #define KS_CASE(LLV) case LLV:                                        \
         if (ksv == 1) KS_LAUNCH(LLV, 2, 1);                           \
         else if (ksv == 2) KS_LAUNCH(LLV, 4, 4);                      \
@@ -1273,15 +1290,16 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
         ra.coef[s] = c->w_Acc + ((size_t)s * 2 * (l + 1) + l) * n;
         ra.base[s] = c->w_Acc + (size_t)s * 2 * (l + 1) * n;
         ra.out[s] = ko.out[s];
-        ra.add[s] = ko.add[s];
+        if (!fold) { ra.add[s] = ko.add[s]; ra.add_g[s] = ko.add_g[s]; ra.acc[s] = ko.acc[s]; }
     }
     ra.coef_pstride = (long long)(l + 1) * n;
     ra.base_pstride = (long long)(l + 1) * n;
     ra.out_pstride = ko.out_pstride;
-    ra.add_pstride = ko.add_pstride;
-    ra.add_pmask = ko.add_pmask;
-    for (int s = 0; s < S; s++) { ra.add_g[s] = ko.add_g[s]; ra.acc[s] = ko.acc[s]; }
-    ra.acc_pstride = ko.acc_pstride;
+    if (!fold) {
+        ra.add_pstride = ko.add_pstride;
+        ra.add_pmask = ko.add_pmask;
+        ra.acc_pstride = ko.acc_pstride;
+    }
     ra.src_id = c->special_id;
     for (u32 i = 0; i < l; i++) { ra.fac[i] = c->pinv[i]; ra.fac_sh[i] = c->pinv_sh[i]; }
     LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));

@@ -216,9 +216,9 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_modup(DigitTab dt, 
     for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(src[C::io(tid, e)], half_j, qj_mod, M);
     const int B = ntt_fwd_row<LOGN, false>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
-    // the inner product accepts lazy digits while l * B * q < 2^64 (128-bit sums stay
-    // below q 2^64, the Montgomery reduction's input bound)
-    if ((u128)l * (u64)B * M.q < ((u128)1 << 64)) {
+    // the inner product accepts lazy digits while (l + 2) B q < 2^64 (its 128-bit sums of
+    // l digit terms and up to two addend terms stay below q 2^64, the Montgomery bound)
+    if ((u128)(l + 2) * (u64)B * M.q < ((u128)1 << 64)) {
         for (int x = tid; x < C::NL; x += C::TH) dst[x] = sm[C::pad(x)];
     } else {
         for (int x = tid; x < C::NL; x += C::TH) dst[x] = red_any(sm[C::pad(x)], M.q, M.mu, M.nq);
@@ -318,10 +318,24 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_rescale(RescaleArgs
 // (group of 4 cts, prime i, coefficient x): the 2l key words are loaded once and
 // reused 4 times; products accumulate in 128 bits and are Montgomery-reduced
 // once per output (sum of l products < l q^2 < q 2^64 for l q < 2^64).
+// Epilogue addends of a key switch, folded into the inner product: ModDown(acc + P y)
+// = ModDown(acc) + y exactly (P y vanishes mod P), so out_p += add_p (read through the
+// automorphism add_g, the c0 of a rotation) and out_p += acc (rotate-and-add) are
+// accumulated here as y * (P R mod q_i) before the Montgomery reduction, and the
+// ModDown rescale kernel only rescales.
+struct KsAdd {
+    const u64 *add[MAXS];         // nullable per s
+    u32 add_g[MAXS];              // != 0: addend of ct s is read through X -> X^g
+    const u64 *acc[MAXS];         // nullable: added to both output polys
+    long long add_pstride, acc_pstride;
+    int add_pmask;                // bit p set: add addend for output poly p
+    u64 pr[MAXQ];                 // P * 2^64 mod q_i (Montgomery form of P)
+};
+
 template <int LL, int KS_GROUP, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, u64 *__restrict__ Acc,
                                                      int S, int L, int logn, int special_id,
-                                                     const ModInfo *__restrict__ mods) {
+                                                     const ModInfo *__restrict__ mods, const KsAdd ka_) {
     constexpr int l = LL;
     const long long n = 1ll << logn;
     const int groups = (S + KS_GROUP - 1) / KS_GROUP;
@@ -363,6 +377,18 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
             for (int j = 0; j < l; j++) {
                 mac128(h0, l0, e[j], kb[j]);
                 mac128(h1, l1, e[j], ka[j]);
+            }
+            if (i < l) {
+                const u64 pr = ka_.pr[i];
+                if (const u64 *ad = ka_.add[s]) {
+                    const long long xa = ka_.add_g[s] ? (long long)galois_perm((u32)x, ka_.add_g[s], logn) : x;
+                    if (ka_.add_pmask & 1) mac128(h0, l0, ad[(long long)i * n + xa], pr);
+                    if (ka_.add_pmask & 2) mac128(h1, l1, ad[ka_.add_pstride + (long long)i * n + xa], pr);
+                }
+                if (const u64 *ac = ka_.acc[s]) {
+                    mac128(h0, l0, ac[(long long)i * n + x], pr);
+                    mac128(h1, l1, ac[ka_.acc_pstride + (long long)i * n + x], pr);
+                }
             }
             Acc[(((long long)s * 2 + 0) * (l + 1) + i) * n + x] = mont_reduce(h0, l0, q, qi);
             Acc[(((long long)s * 2 + 1) * (l + 1) + i) * n + x] = mont_reduce(h1, l1, q, qi);
