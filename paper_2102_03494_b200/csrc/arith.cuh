@@ -26,6 +26,7 @@ struct ModInfo {
     u64 r2;        // 2^128 mod q
     u64 mu;        // floor(2^64 / q)
     u64 ninv, ninv_sh;
+    u64 w1ninv, w1ninv_sh;     // (last inverse-NTT twiddle) * n^-1: the scaling folds into the last stage
     u64 half;      // (q - 1) / 2
     u64 nq;        // -q mod 2^64 (the quotient subtraction folds into a multiply-add)
     u64 q3;        // 3q, loaded (not derived) so ptxas keeps it in a register instead of
@@ -46,7 +47,7 @@ DEV u64 shoup(u64 a, u64 w, u64 wsh, u64 q) {
 // (it only carries at most 1 into the high word).  5 IMADs instead of 7.
 DEV u64 mulhi_approx(u64 a, u64 b) {
     const u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
-    u32 t0, t1, t2;
+    u32 t0, t1, t2;       // t0: low word, only its carry is used
     asm("mul.lo.u32 %0, %4, %5;\n\t"
         "mul.hi.u32 %1, %4, %5;\n\t"
         "mad.lo.cc.u32 %0, %3, %6, %0;\n\t"
@@ -56,7 +57,6 @@ DEV u64 mulhi_approx(u64 a, u64 b) {
         "madc.hi.u32 %2, %4, %6, %2;"
         : "=&r"(t0), "=&r"(t1), "=&r"(t2)
         : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
-    (void)t0;
     return ((u64)t2 << 32) | t1;
 }
 // a*w mod q in [0, 3q) for any 64-bit a (Shoup with the approximate quotient);

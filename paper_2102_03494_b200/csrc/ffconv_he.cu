@@ -488,6 +488,8 @@ static int setup_moduli(fhe_ctx *c) {
         M.mu = (u64)(((u128)1 << 64) / q);
         M.ninv = hm::inv(n, q);
         M.ninv_sh = hm::shoup(M.ninv, q);
+        M.w1ninv = hm::mul(pwi[hm::brev(1, c->logn)], M.ninv, q);
+        M.w1ninv_sh = hm::shoup(M.w1ninv, q);
         M.half = (q - 1) / 2;
         M.nq = (u64)0 - q;
         M.q3 = 3 * q;

@@ -7,12 +7,13 @@
 //
 // Layout: every thread owns E = 2^W words in registers and runs up to W
 // butterfly stages per pass; passes exchange through shared memory padded one
-// word per 2^W (conflict-free for 64-bit accesses).  n >= 2^12 uses W = 5
-// (radix-32, 512 threads x 128 registers for n = 2^14, 132 KB of shared memory)
-// for inverse transforms, W = 4 (1024 x 64) for forward ones: standalone 46 % / 40 %
-// of the integer peak (fwd W5 / inv W5) vs 45 % / 35 % at W = 4, but the fused
-// forward kernels (ModUp, rescale) run faster at W = 4 (profiles/r01_*).  Values are kept lazily in [0, 4q)
-// (forward, Harvey) / [0, 2q) (inverse) and reduced once at the end.
+// word per 2^W (conflict-free for 64-bit accesses).  Default W = 4 (radix-16,
+// 1024 threads x 64 registers for n = 2^14, 139 KB of shared memory) for both
+// directions: standalone, W = 5 is 2-5 % faster, but inside the fused row kernels
+// (ModUp, ModDown, the rotation's gather + INTT) W = 4 wins -- the radix-32 inverse
+// kernels are ~105 KB of SASS and stall on instruction fetch (profiles/r01_*).
+// Butterfly values are kept lazily bounded (FwdLazy / InvLazy below) and reduced
+// once at the end.
 #pragma once
 #include "arith.cuh"
 
@@ -66,13 +67,20 @@ struct InvLazy {
         a = U + V;
         b = shoup_approx(U - V + Bq, tw.x, tw.y, nq);
     }
+    // last stage (one twiddle w1 for every butterfly) with the n^-1 scaling folded in:
+    // canonical outputs (U + V) n^-1 and (U - V) w1 n^-1
+    DEV void last(u64 &a, u64 &b, const ModInfo &M) const {
+        const u64 U = a, V = b;
+        a = shoup(U + V, M.ninv, M.ninv_sh, q);
+        b = shoup(U - V + Bq, M.w1ninv, M.w1ninv_sh, q);
+    }
 };
 
 #ifndef NTT_W_FWD
 #define NTT_W_FWD 4
 #endif
 #ifndef NTT_W_INV
-#define NTT_W_INV 5
+#define NTT_W_INV 4
 #endif
 
 // default radix per pass: 2^5 (512 threads, 32 words each) for the large rings,
@@ -164,7 +172,6 @@ template <int LOGN, int WW = DefaultWInv<LOGN>::value>
 DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid, u32 g_perm = 0) {
     using C = NttCfg<LOGN, WW>;
     constexpr int W = C::W, E = C::E, NP = C::NP, N = C::N;
-    const u64 q = M.q;
     InvLazy Lz(M);
 #pragma unroll
     for (int p = 0; p < NP; p++) {
@@ -185,6 +192,12 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
             const int b = lt - f0;
             const int h = N >> (lt + 1);
             Lz.stage();
+            if (lt == LOGN - 1) {          // last stage: twiddle itw[1] for all, n^-1 folded in
+#pragma unroll
+                for (int e = 0; e < E; e++)
+                    if (!(e & (1 << b))) Lz.last(v[e], v[e | (1 << b)], M);
+                continue;
+            }
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
@@ -204,8 +217,6 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
             __syncthreads();
         }
     }
-#pragma unroll
-    for (int e = 0; e < E; e++) v[e] = shoup(v[e], M.ninv, M.ninv_sh, q);
 }
 
 
@@ -326,7 +337,6 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
     namespace cg = cooperative_groups;
     using R = RowCfg<LOGN, true>;
     constexpr int W = R::W, E = R::E, LOGL = R::LOGL, CL = R::CL, N = R::N;
-    const u64 q = M.q;
     InvLazy Lz(M);
     const int rank = R::rank(), gtid = rank * R::TH + tid;
     cg::cluster_group cl = cg::this_cluster();
@@ -375,6 +385,12 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
     for (int b = 0; b < W; b++) {
         const int lt = LOGN - W + b;
         Lz.stage();
+        if (lt == LOGN - 1) {              // last stage: n^-1 folded in
+#pragma unroll
+            for (int e = 0; e < E; e++)
+                if (!(e & (1 << b))) Lz.last(v[e], v[e | (1 << b)], M);
+            continue;
+        }
 #pragma unroll
         for (int e = 0; e < E; e++) {
             if (e & (1 << b)) continue;
@@ -388,8 +404,6 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
         }
     }
     cl.sync();   // no CTA leaves or reuses its shared memory while another reads it
-#pragma unroll
-    for (int e = 0; e < E; e++) v[e] = shoup(v[e], M.ninv, M.ninv_sh, q);
 }
 
 // Row-size dispatch used by the row kernels.
