@@ -5,6 +5,8 @@ words to both and compares outputs word for word, plus decrypted slots against
 plain modular arithmetic (the reference slot semantics, hesim.py:244-345).
 """
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -20,6 +22,13 @@ CASES = [
     (1024, [786433, 65537], 4, 55),
     (8192, [65537], 5, 55),
     (8192, [1099511922689], 4, 40),
+    # lazy-bound classes of the butterfly schedule (LIM = 2^clz(q)): q < 2^58 never reduces a
+    # forward stage, 60-bit primes (LIM = 16) every other one, the 61-bit special prime
+    # (LIM = 8) nearly all; 7 levels of 61-bit primes (LIM = 8 everywhere) take the
+    # canonical-ModUp and the rescale-addend fallbacks ((l + 2) q >= 2^64)
+    (1024, [65537], 3, 58),
+    (8192, [65537], 3, 60),
+    (64, [65537], 7, 61),
     # rings 2^15 / 2^16: one row per thread-block cluster of 2 / 4 CTAs (DSMEM NTT)
     (16384, [65537], 3, 50),
     (32768, [786433], 3, 50),
@@ -30,6 +39,9 @@ BIG = CASES[-2:]
 def _pair(case, golden_lib, cuda_lib):
     n_slots, t, L, qb = case
     P = make_params(n_slots, t, levels=L, q_bits=qb)
+    if qb == 61:                      # 61-bit q: the largest of the L + 1 primes is the special one
+        ps = sorted(P.q + P.p, reverse=True)
+        P = dataclasses.replace(P, q=tuple(ps[1:]), p=(ps[0],))
     return Evaluator(P, golden_lib), Evaluator(P, cuda_lib), P
 
 
