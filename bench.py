@@ -237,11 +237,11 @@ def run_rotation(args, rank, world, local_rank):
     lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt1))
     launches = int((cnt1.value - cnt0.value) * args.steps / (args.steps + args.warmup))
 
-    # secondary rates: HMA (acc += rot * pt) and rescale
+    # secondary rates: HMA (acc += ct * pt, one fused in-place kernel) and rescale
     acc = {"a": ev.zero(B)}
 
     def hma_step():
-        acc["a"] = ev.add(acc["a"], ev.mul_plain(ct, pt))
+        ev.mul_plain_acc(ct, pt, acc["a"])
 
     hma_ms = timed(hma_step, args.steps, args.warmup)
 

@@ -145,6 +145,8 @@ int fhe_decrypt_raw(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *coef);
 /* ---- evaluation (out may alias an input unless stated) --------------------- */
 int fhe_add(fhe_ctx *ctx, const fhe_ct *a, const fhe_ct *b, fhe_ct *out);
 int fhe_mul_plain(fhe_ctx *ctx, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out);
+/* fused HMA: acc += a * pt in place (= fhe_add(acc, fhe_mul_plain(a, pt)); acc must not alias a) */
+int fhe_mul_plain_acc(fhe_ctx *ctx, const fhe_ct *a, const fhe_pt *pt, fhe_ct *acc);
 int fhe_mul_scalar(fhe_ctx *ctx, const fhe_ct *a, int64_t w, fhe_ct *out);
 int fhe_add_plain(fhe_ctx *ctx, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out);
 /* left rotation of both rows by k in [1, N): Galois element 5^k mod 2n, then

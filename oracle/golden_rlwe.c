@@ -780,6 +780,22 @@ int fhe_mul_plain(fhe_ctx *c, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out) {
     return 0;
 }
 
+int fhe_mul_plain_acc(fhe_ctx *c, const fhe_ct *a, const fhe_pt *pt, fhe_ct *acc) {
+    if (!same_shape(a, acc)) return fail(FHE_ELEVEL, "mul_plain_acc: shape/level mismatch");
+    if (a == acc) return fail(FHE_EINVAL, "mul_plain_acc: the accumulator must not alias the input");
+    for (u32 ci = 0; ci < a->count; ci++) {
+        u32 k = ci / a->R;
+        for (u32 p = 0; p < 2; p++)
+            for (u32 i = 0; i < a->level; i++) {
+                u64 q = c->P.q[i];
+                const u64 *x = poly(a, ci, p, i), *w = pt->ntt_q + ((size_t)k * c->L + i) * c->n;
+                u64 *z = poly(acc, ci, p, i);
+                for (u32 j = 0; j < c->n; j++) z[j] = addmod(z[j], mulmod(x[j], w[j], q), q);
+            }
+    }
+    return 0;
+}
+
 int fhe_mul_scalar(fhe_ctx *c, const fhe_ct *a, int64_t w, fhe_ct *out) {
     if (!same_shape(a, out)) return fail(FHE_ELEVEL, "mul_scalar: shape/level mismatch");
     for (u32 ci = 0; ci < a->count; ci++)

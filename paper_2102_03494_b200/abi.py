@@ -80,6 +80,7 @@ SIGNATURES = {
     "fhe_decrypt_raw": (c_int, [c_void_p, c_void_p, _U64P]),
     "fhe_add": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fhe_mul_plain": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "fhe_mul_plain_acc": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fhe_mul_scalar": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "fhe_add_plain": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fhe_rotate": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p]),

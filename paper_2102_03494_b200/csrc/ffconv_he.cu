@@ -1169,14 +1169,28 @@ extern "C" int fhe_add(fhe_ctx *c, const fhe_ct *a, const fhe_ct *b, fhe_ct *out
     return 0;
 }
 
+static int mul_plain_rows(fhe_ctx *c, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out, const u64 *acc) {
+    const int rows = (int)(a->count * 2 * a->level);
+    const unsigned bx = (unsigned)std::max<size_t>(1, (c->n / 2 + 255) / 256);
+    dim3 grid(bx, (unsigned)std::min(rows, 65535));
+    ProfScope ps_(c, "k_mul_plain");
+    k_mul_plain<<<grid, 256, 0, c->st>>>(a->d, pt->ntt_m, out->d, acc, rows, (int)a->level, (int)c->L, (int)a->R,
+                                        (int)c->logn, c->d_mods);
+    CHECK_LAUNCH();
+    return 0;
+}
+
 extern "C" int fhe_mul_plain(fhe_ctx *c, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out) {
     if (!same_shape(a, out)) return fail(FHE_ELEVEL, "mul_plain: shape/level mismatch");
     if (!pt->encoded) return fail(FHE_EINVAL, "mul_plain: plaintext was never encoded");
-    long long total = (long long)ct_words(a);
-    EW(k_mul_plain, total, a->d, pt->ntt_m, out->d, total, (int)a->level, (int)c->L, (int)a->R, (int)c->logn,
-       c->d_mods);
-    CHECK_LAUNCH();
-    return 0;
+    return mul_plain_rows(c, a, pt, out, nullptr);
+}
+
+extern "C" int fhe_mul_plain_acc(fhe_ctx *c, const fhe_ct *a, const fhe_pt *pt, fhe_ct *acc) {
+    if (!same_shape(a, acc)) return fail(FHE_ELEVEL, "mul_plain_acc: shape/level mismatch");
+    if (!pt->encoded) return fail(FHE_EINVAL, "mul_plain_acc: plaintext was never encoded");
+    if (a == acc) return fail(FHE_EINVAL, "mul_plain_acc: the accumulator must not alias the input");
+    return mul_plain_rows(c, a, pt, acc, acc->d);
 }
 
 extern "C" int fhe_mul_scalar(fhe_ctx *c, const fhe_ct *a, int64_t w, fhe_ct *out) {

@@ -406,17 +406,28 @@ __global__ void k_add(const u64 *__restrict__ a, const u64 *__restrict__ b, u64 
 }
 
 // out[ci][p][i] = a[ci][p][i] * pt[k][i] (pt Montgomery form, k = ci / R)
-__global__ void k_mul_plain(const u64 *__restrict__ a, const u64 *__restrict__ ptm, u64 *__restrict__ out,
-                            long long total, int l, int L, int R, int logn, const ModInfo *__restrict__ mods) {
+// out[ci][p][i] = a[ci][p][i] * pt[k][i] (+ acc[ci][p][i]) (pt Montgomery form, k = ci / R).
+// One polynomial row (ci, p, i) per blockIdx.y (no per-element index divisions),
+// two words per thread (16-byte accesses).
+__global__ void k_mul_plain(const u64 *__restrict__ a, const u64 *__restrict__ ptm, u64 *out, const u64 *acc,
+                            int rows, int l, int L, int R, int logn, const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
-    GRID_STRIDE(idx, total) {
-        const long long row = idx >> logn;
-        const int i = (int)(row % l);
-        const long long ci = row / (2 * l);
-        const int k = (int)(ci / R);
+    const long long x = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+    if (x >= n) return;
+    for (int row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = row % l, ci = row / (2 * l), k = ci / R;
         const ModInfo &M = mods[i];
-        const u64 w = __ldg(ptm + ((long long)k * L + i) * n + (idx & (n - 1)));
-        out[idx] = mont(a[idx], w, M.q, M.qinv);
+        const u64 q = M.q, qi = M.qinv;
+        const long long off = (long long)row * n + x;
+        const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(a + off);
+        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2 *>(ptm + ((long long)k * L + i) * n + x));
+        u64 r0 = mont(av.x, w.x, q, qi), r1 = mont(av.y, w.y, q, qi);
+        if (acc) {
+            const ulonglong2 cv = *reinterpret_cast<const ulonglong2 *>(acc + off);
+            r0 = addm(r0, cv.x, q);
+            r1 = addm(r1, cv.y, q);
+        }
+        *reinterpret_cast<ulonglong2 *>(out + off) = make_ulonglong2(r0, r1);
     }
 }
 

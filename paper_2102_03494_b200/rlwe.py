@@ -180,6 +180,11 @@ class Evaluator:
         self.lib.call("fhe_mul_plain", self.ctx, a.ptr, pt.ptr, out.ptr)
         return out
 
+    def mul_plain_acc(self, a: Ciphertext, pt: Plaintext, acc: Ciphertext) -> Ciphertext:
+        """acc += a * pt in place (fused HMA); returns acc."""
+        self.lib.call("fhe_mul_plain_acc", self.ctx, a.ptr, pt.ptr, acc.ptr)
+        return acc
+
     def mul_scalar(self, a: Ciphertext, w: int, out: Ciphertext | None = None) -> Ciphertext:
         out = out or self.new_ct(a.rows, a.level)
         self.lib.call("fhe_mul_scalar", self.ctx, a.ptr, int(w), out.ptr)

@@ -88,6 +88,13 @@ def test_ops_bit_exact(pair):
     same(gd.add(ag, bg), gp.add(ac, bc), (A + B) % t)
     same(gd.mul_plain(ag, ptg), gp.mul_plain(ac, ptc), (A * pts.astype(object)[:, None, :]) % t)
     same(gd.mul_scalar(ag, -5), gp.mul_scalar(ac, -5), (A * -5) % t)
+    # fused HMA: acc += a * pt in place == add(acc, mul_plain(a, pt))
+    accg, accc = gd.encrypt(b_s, nonce=2), gp.new_ct(R)
+    gp.write(accc, gd.read(accg))
+    gd.mul_plain_acc(ag, ptg, accg)
+    gp.mul_plain_acc(ac, ptc, accc)
+    same(accg, accc, (B + A * pts.astype(object)[:, None, :]) % t)
+    assert np.array_equal(gp.read(accc), gp.read(gp.add(bc, gp.mul_plain(ac, ptc))))
     same(gd.add_plain(ag, ptg), gp.add_plain(ac, ptc), (A + pts.astype(object)[:, None, :]) % t)
     N = P.n_slots
     for k in sorted({1, N // 2 + 1, N - 1} & set(range(1, N))):
