@@ -163,8 +163,8 @@ struct fhe_ctx {
     int enc_next = 0;
     // workspaces (key switching: two ping-pong sets, one per stream)
     int S = 1;                          // key-switching sub-batch
-    u64 *w_D = nullptr, *w_C1 = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;   // current set
-    u64 *ws_D[2]{}, *ws_C1[2]{}, *ws_Ext[2]{}, *ws_Acc[2]{};
+    u64 *w_D = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;   // current set
+    u64 *ws_D[2]{}, *ws_Ext[2]{}, *ws_Acc[2]{};
     cudaStream_t streams[2]{};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_key = nullptr;
     u64 *w_sq = nullptr;
@@ -538,7 +538,7 @@ static int setup_secret(fhe_ctx *c) {
 
 static int setup_workspace(fhe_ctx *c) {
     size_t n = c->n, L = c->L;
-    size_t per_ct = n * (2 * L + L * (L + 1) + 2 * (L + 1)) * 8;
+    size_t per_ct = n * (L + L * (L + 1) + 2 * (L + 1)) * 8;
     size_t budget = 512ull << 20;
     const char *env = getenv("FHE_KS_BATCH");
     int S = env ? atoi(env) : (int)(budget / per_ct);
@@ -548,11 +548,10 @@ static int setup_workspace(fhe_ctx *c) {
     c->S = S;
     for (int k = 0; k < 2; k++) {
         CU(cudaMalloc((void **)&c->ws_D[k], S * L * n * 8));
-        CU(cudaMalloc((void **)&c->ws_C1[k], S * L * n * 8));
         CU(cudaMalloc((void **)&c->ws_Ext[k], S * L * (L + 1) * n * 8));
         CU(cudaMalloc((void **)&c->ws_Acc[k], S * 2 * (L + 1) * n * 8));
     }
-    c->w_D = c->ws_D[0]; c->w_C1 = c->ws_C1[0]; c->w_Ext = c->ws_Ext[0]; c->w_Acc = c->ws_Acc[0];
+    c->w_D = c->ws_D[0]; c->w_Ext = c->ws_Ext[0]; c->w_Acc = c->ws_Acc[0];
     CU(cudaStreamCreateWithFlags(&c->streams[1], cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -660,7 +659,7 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
                     c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_sq};
     for (void *b : bufs) if (b) cudaFree(b);
     for (int k = 0; k < 2; k++) {
-        void *wb[] = {c->ws_D[k], c->ws_C1[k], c->ws_Ext[k], c->ws_Acc[k]};
+        void *wb[] = {c->ws_D[k], c->ws_Ext[k], c->ws_Acc[k]};
         for (void *b : wb) if (b) cudaFree(b);
     }
     if (c->streams[1]) { cudaStreamSynchronize(c->streams[1]); cudaStreamDestroy(c->streams[1]); }
@@ -1331,7 +1330,7 @@ static int keyswitch_core(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
 // rotate a list of physical ciphertexts (each [2][l][n]) by Galois element g
 static void use_lane(fhe_ctx *c, int k) {
     c->st = c->streams[k];
-    c->w_D = c->ws_D[k]; c->w_C1 = c->ws_C1[k]; c->w_Ext = c->ws_Ext[k]; c->w_Acc = c->ws_Acc[k];
+    c->w_D = c->ws_D[k]; c->w_Ext = c->ws_Ext[k]; c->w_Acc = c->ws_Acc[k];
 }
 
 // rotate a list of physical ciphertexts (each [2][l][n]), ciphertext i by
@@ -1366,7 +1365,7 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
         memset(&pt, 0, sizeof pt);
         for (int s = 0; s < S; s++) { pt.in[s] = in[b0 + s]; pt.out[s] = out[b0 + s]; pt.g[s] = g[b0 + s]; }
         LOGN_SWITCH(c->logn, launch_row<LG, true>(c, "k_rot_gather_intt", k_rot_gather_intt<LG>, dim3(S, l), c->st,
-                                                  pt, (int)l, c->w_C1, c->w_D, c->d_mods));
+                                                  pt, (int)l, c->w_D, c->d_mods));
         if (cudaGetLastError() != cudaSuccess) { rc = fail(FHE_EDEVICE, "k_rot_gather_intt launch failed"); break; }
         DigitTab dt;
         KsOut ko;
@@ -1374,7 +1373,8 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
         memset(&ko, 0, sizeof ko);
         for (int s = 0; s < S; s++) {
             dt.coef[s] = c->w_D + (size_t)s * l * n;
-            dt.ntt[s] = c->w_C1 + (size_t)s * l * n;
+            dt.ntt[s] = in[b0 + s] + (size_t)l * n;      // c1 limbs, read through the automorphism
+            dt.dperm[s] = g[b0 + s];
             dt.key[s] = keys[b0 + s];
             ko.out[s] = out[b0 + s];
             ko.add[s] = in[b0 + s];          // c0 limbs, read through the automorphism
@@ -1487,7 +1487,7 @@ extern "C" int fhe_rotate_hoisted(fhe_ctx *c, const fhe_ct *a, const uint32_t *k
         memset(&pt, 0, sizeof pt);
         for (int s = 0; s < si; s++) { pt.in[s] = a->d + (b0 + s) * stride; pt.out[s] = nullptr; pt.g[s] = 1; }
         LOGN_SWITCH(c->logn, launch_row<LG, true>(c, "k_rot_gather_intt", k_rot_gather_intt<LG>, dim3(si, l), c->st,
-                                                  pt, (int)l, c->w_C1, c->w_D, c->d_mods));
+                                                  pt, (int)l, c->w_D, c->d_mods));
         CHECK_LAUNCH();
         DigitTab dm;
         memset(&dm, 0, sizeof dm);
@@ -1511,6 +1511,7 @@ extern "C" int fhe_rotate_hoisted(fhe_ctx *c, const fhe_ct *a, const uint32_t *k
                 dt.ntt[it] = src + (size_t)l * n;      // c1 limbs, natural NTT order (diagonal digits)
                 dt.key[it] = key;
                 dt.perm[it] = g[j];
+                dt.dperm[it] = g[j];
                 dt.esrc[it] = s;
                 ko.out[it] = out[j]->d + (b0 + s) * stride;
                 ko.add[it] = src;                      // c0 limbs, read through the automorphism

@@ -150,12 +150,12 @@ struct PtrTab {
     u32 g[MAXS];          // Galois element per ciphertext
 };
 
-// Key switching, step 1 (rotation).  grid (S, l): c1 limb i of input ct s.
-// The row is staged in shared memory once; the automorphism is applied as a
-// gather on the way out (C1p[s][i]: NTT-form digit for the inner-product
-// diagonal) and on the first inverse-NTT pass (D[s][i]: coefficient digit).
+// Key switching, step 1 (rotation).  grid (S, l): c1 limb i of input ct s, staged in
+// shared memory; the automorphism is applied on the first inverse-NTT pass
+// (D[s][i]: coefficient digit).  The inner product reads its diagonal (the NTT-form
+// digit tau_g(c1)_i) straight from the input through the same automorphism.
 template <int LOGN>
-__global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_rot_gather_intt(PtrTab pt, int l, u64 *C1p, u64 *D,
+__global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_rot_gather_intt(PtrTab pt, int l, u64 *D,
                                                                       const ModInfo *__restrict__ mods) {
     using C = RowCfg<LOGN, true>;
     extern __shared__ u64 sm[];
@@ -163,21 +163,15 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_rot_gather_intt(PtrT
     const long long n = C::N;
     const u32 g = pt.g[s];
     const u64 *src = pt.in[s] + ((long long)l + i) * n;
-    u64 *side = C1p + ((long long)s * l + i) * n;
     const ModInfo M = mods[i];
     u64 v[C::E];
     if constexpr (C::CL == 0) {
         for (int x = tid; x < C::NL; x += C::TH) sm[C::pad(x)] = src[x];
         __syncthreads();
-        for (int x = tid; x < C::NL; x += C::TH) side[x] = sm[C::pad(galois_perm(x, g, LOGN))];
         ntt_inv_core<LOGN>(v, sm, M, tid, g);
     } else {
         // cluster row: the automorphism gathers across CTAs, so read it from global memory
-        for (int x = tid; x < C::NL; x += C::TH) {
-            const u64 w = src[galois_perm(base + x, g, LOGN)];
-            side[base + x] = w;
-            sm[C::pad(x)] = w;
-        }
+        for (int x = tid; x < C::NL; x += C::TH) sm[C::pad(x)] = src[galois_perm(base + x, g, LOGN)];
         __syncthreads();
         ntt_inv_row<LOGN>(v, sm, M, tid);
     }
@@ -193,6 +187,7 @@ struct DigitTab {
     u32 perm[MAXS];          // != 0: hoisted rotation -- the extended digits are read through the
                              // NTT-domain automorphism by this Galois element ...
     u32 esrc[MAXS];          // ... from Ext block esrc[s] (rotations of one input share its ModUp)
+    u32 dperm[MAXS];         // != 0: the diagonal digit is read from ntt[s] through X -> X^dperm
 };
 
 // Key switching, step 2 (ModUp).  grid (S, l, l+1): digit j of ct s lifted (centered)
@@ -367,11 +362,12 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
             }
             // hoisted rotations share one ModUp: Ext(tau_g(c1)) = Ext(c1) read at perm_g(x)
             const long long xs = dt.perm[s] ? (long long)galois_perm((u32)x, dt.perm[s], logn) : x;
+            const long long xd = dt.dperm[s] ? (long long)galois_perm((u32)x, dt.dperm[s], logn) : x;
             const int es = dt.perm[s] ? (int)dt.esrc[s] : s;
             u64 e[l];
 #pragma unroll
             for (int j = 0; j < l; j++)
-                e[j] = i == j ? dt.ntt[s][(long long)j * n + xs] : Ext[((((long long)es * l + j) * (l + 1)) + i) * n + xs];
+                e[j] = i == j ? dt.ntt[s][(long long)j * n + xd] : Ext[((((long long)es * l + j) * (l + 1)) + i) * n + xs];
             u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
 #pragma unroll
             for (int j = 0; j < l; j++) {
