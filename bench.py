@@ -907,7 +907,8 @@ def main():
         hinf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=1, warmup=1,
                              schedule="hoisted")
         res["inference_hoisted"] = {k: hinf[k] for k in ("schedule", "images_per_s", "e2e_images_per_s",
-                                                         "logical_rotations_per_chunk", "kernel_ms_one_chunk")}
+                                                         "logical_rotations_per_chunk", "roofline",
+                                                         "kernel_ms_one_chunk")}
         res["rates"]["images_per_s_hoisted"] = hinf["images_per_s"]
     if rank == 0 and world == 1:
         rate, sample = cpu_baseline_rotation(1, seconds=3.0)
