@@ -396,12 +396,11 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
 __global__ void k_add(const u64 *__restrict__ a, const u64 *__restrict__ b, u64 *__restrict__ out, long long total,
                       int l, int logn, const ModInfo *__restrict__ mods) {
     GRID_STRIDE(idx, total) {
-        const int i = (int)((idx >> logn) % l);
+        const int i = (int)((u32)(idx >> logn) % (u32)l);
         out[idx] = addm(a[idx], b[idx], mods[i].q);
     }
 }
 
-// out[ci][p][i] = a[ci][p][i] * pt[k][i] (pt Montgomery form, k = ci / R)
 // out[ci][p][i] = a[ci][p][i] * pt[k][i] (+ acc[ci][p][i]) (pt Montgomery form, k = ci / R).
 // One polynomial row (ci, p, i) per blockIdx.y (no per-element index divisions),
 // two words per thread (16-byte accesses).
@@ -440,13 +439,19 @@ __global__ void k_mul_scalar(const u64 *__restrict__ a, u64 *__restrict__ out, l
 
 // round(Q_l m / t_k) mod q_i for a coefficient m in [0, t_k):
 // Delta*m + round(rt*m/t) with Delta = floor(Q_l/t_k), rt = Q_l mod t_k.
-DEV u64 scaled_msg(const LevelDev &T, int k, u64 t, u64 m, int i, const ModInfo &Mq) {
+// round(rt m / t), the part of round(Q m / t) = Delta m + round(rt m / t) that does not depend on q_i
+DEV u64 scaled_corr(const LevelDev &T, int k, u64 t, u64 m) {
     const u64 rt = T.rt[k];
     u64 est = mulhi(m, T.rtF[k]);                        // floor(rt m / t) - {0,1}
     u128 rem = (u128)rt * m - (u128)est * t;
     while (rem >= t) { rem -= t; est++; }
-    const u64 corr = est + (2 * (u64)rem >= t ? 1 : 0);
+    return est + (2 * (u64)rem >= t ? 1 : 0);
+}
+DEV u64 scaled_msg_i(const LevelDev &T, int k, u64 m, u64 corr, int i, const ModInfo &Mq) {
     return addm(mont(red64(m, Mq.q, Mq.mu), T.delta_m[k][i], Mq.q, Mq.qinv), red64(corr, Mq.q, Mq.mu), Mq.q);
+}
+DEV u64 scaled_msg(const LevelDev &T, int k, u64 t, u64 m, int i, const ModInfo &Mq) {
+    return scaled_msg_i(T, k, m, scaled_corr(T, k, t, m), i, Mq);
 }
 
 // rows [count][l][n] (or [T][l][n] with R = 1): out = NTT-pending scaled message
@@ -455,11 +460,12 @@ __global__ void k_scaled_msg(const u64 *__restrict__ m, u64 *__restrict__ out, l
                              int logn, const LevelDev *__restrict__ T, int t_id0, const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
     GRID_STRIDE(idx, total) {
-        const long long row = idx >> logn;
-        const int i = (int)(row % l);
-        const int k = (int)(row / l / R);
+        const u32 row = (u32)(idx >> logn);
+        const int i = (int)(row % (u32)l);
+        const u32 ci = row / (u32)l;
+        const int k = (int)(ci / (u32)R);
         const long long x = idx & (n - 1);
-        out[idx] = scaled_msg(*T, k, mods[t_id0 + k].q, m[(row / l) * n + x], i, mods[i]);
+        out[idx] = scaled_msg(*T, k, mods[t_id0 + k].q, m[(long long)ci * n + x], i, mods[i]);
     }
 }
 
@@ -471,9 +477,9 @@ __global__ void k_enc_prep(const u64 *__restrict__ m, u64 *__restrict__ tmp, lon
                            const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
     GRID_STRIDE(idx, total8) {
-        const long long per = (n + 7) >> 3;               // 8-coefficient groups per ciphertext
-        const u32 ci = (u32)(idx / per);
-        const u32 x0 = (u32)(idx % per) * 8;
+        const int lper = logn > 3 ? logn - 3 : 0;           // log2 of the 8-coefficient groups per ciphertext
+        const u32 ci = (u32)(idx >> lper);
+        const u32 x0 = (u32)(idx & ((1ll << lper) - 1)) * 8;
         const int k = (int)(ci / R);
         u32 blk[16];
         chacha_block(blk, seed, x0 >> 3, DOM_ENC_E, 0, nonce, ci);
@@ -482,12 +488,19 @@ __global__ void k_enc_prep(const u64 *__restrict__ m, u64 *__restrict__ tmp, lon
         for (int u = 0; u < 8; u++)
             e[u] = __popc(blk[2 * u] & 0x1FFFFFu) - __popc(blk[2 * u + 1] & 0x1FFFFFu);
         const u64 t = mods[t_id0 + k].q;
+        u64 mv[8], corr[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            mv[u] = x0 + u < n ? m[(long long)ci * n + x0 + u] : 0;
+            corr[u] = scaled_corr(*T, k, t, mv[u]);
+        }
         for (int i = 0; i < L; i++) {
             const ModInfo &M = mods[i];
             u64 *dst = tmp + ((long long)ci * L + i) * n + x0;
 #pragma unroll
             for (int u = 0; u < 8; u++)
-                if (x0 + u < n) dst[u] = addm(smod(e[u], M), scaled_msg(*T, k, t, m[(long long)ci * n + x0 + u], i, M), M.q);
+                if (x0 + u < n) dst[u] = addm(e[u] >= 0 ? (u64)e[u] : M.q - (u64)(-e[u]),     // |e| <= 21 < q
+                                             scaled_msg_i(*T, k, mv[u], corr[u], i, M), M.q);
         }
     }
 }
@@ -499,11 +512,11 @@ __global__ void k_enc_finish(const u64 *__restrict__ tmp, u64 *__restrict__ ct, 
                              long long total4, int L, int logn, u64 seed, u32 nonce, const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
     GRID_STRIDE(idx, total4) {
-        const long long per = (n + 3) >> 2;
-        const long long row = idx / per;                   // ci * L + i
-        const int i = (int)(row % L);
-        const u32 ci = (u32)(row / L);
-        const u32 x0 = (u32)(idx % per) * 4;
+        const int lper = logn > 2 ? logn - 2 : 0;           // log2 of the 4-coefficient groups per row
+        const u32 row = (u32)(idx >> lper);                 // ci * L + i
+        const int i = (int)(row % (u32)L);
+        const u32 ci = row / (u32)L;
+        const u32 x0 = (u32)(idx & ((1ll << lper) - 1)) * 4;
         const ModInfo &M = mods[i];
         u32 blk[16];
         chacha_block(blk, seed, x0 >> 2, DOM_ENC_A, i, nonce, ci);
@@ -516,7 +529,7 @@ __global__ void k_enc_finish(const u64 *__restrict__ tmp, u64 *__restrict__ ct, 
                            blk[4 * u];
             const u64 a = mod128(v, M);
             const u64 as = mont(a, s_m[(long long)i * n + x], M.q, M.qinv);
-            c[((long long)0 * L + i) * n + x] = subm(tmp[row * n + x], as, M.q);
+            c[((long long)0 * L + i) * n + x] = subm(tmp[(long long)row * n + x], as, M.q);
             c[((long long)1 * L + i) * n + x] = a;
         }
     }
@@ -527,9 +540,9 @@ __global__ void k_dec_mul(const u64 *__restrict__ ct, const u64 *__restrict__ s_
                           long long total, int l, int logn, const ModInfo *__restrict__ mods) {
     const long long n = 1ll << logn;
     GRID_STRIDE(idx, total) {
-        const long long row = idx >> logn;
-        const int i = (int)(row % l);
-        const long long ci = row / l;
+        const u32 row = (u32)(idx >> logn);
+        const int i = (int)(row % (u32)l);
+        const long long ci = row / (u32)l;
         const long long x = idx & (n - 1);
         const ModInfo &M = mods[i];
         const u64 *c = ct + ci * 2 * l * n;
@@ -545,7 +558,7 @@ __global__ void k_dec_scale(const u64 *__restrict__ X, u64 *__restrict__ m, long
     GRID_STRIDE(idx, total) {
         const long long ci = idx >> logn;
         const long long x = idx & (n - 1);
-        const int k = (int)(ci / R);
+        const int k = (int)((u32)ci / (u32)R);
         u128 ai = 0, af = 0;
         for (int i = 0; i < l; i++) {
             const ModInfo &M = mods[i];
