@@ -95,6 +95,25 @@ struct DefaultWInv {   // inverse transforms
 };
 
 
+// The twiddles of one stage for one thread are D = 2^(W - b - 1) consecutive table
+// entries starting at an even index (b: the stage's butterfly bit within the thread's
+// words); pairs of (w, w') entries are fetched with one 256-bit load.
+DEV void ldg_tw2(const ulonglong2 *p, ulonglong2 &a, ulonglong2 &b) {
+    asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(a.x), "=l"(a.y), "=l"(b.x), "=l"(b.y)
+        : "l"(p));
+}
+template <int ND>
+DEV void fetch_tw(ulonglong2 (&tw)[ND], const ulonglong2 *p, int D) {
+    if (D == 1) {
+        tw[0] = __ldg(p);
+    } else {
+#pragma unroll
+        for (int d = 0; d < ND; d += 2)
+            if (d < D) ldg_tw2(p + d, tw[d], tw[d + 1]);
+    }
+}
+
 template <int LOGN, int WW = DefaultW<LOGN>::value>
 struct NttCfg {
     static constexpr int N = 1 << LOGN;
@@ -146,12 +165,12 @@ DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, i
                 for (int e = 0; e < E; e++)
                     if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
             }
+            ulonglong2 tw[E / 2];
+            fetch_tw(tw, M.tw + (1u << s) + ((u32)fidx<W>(tid, 0, f0) >> (LOGN - s)), E >> (b + 1));
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
-                const int e2 = e | (1 << b);
-                const u32 g = (1u << s) + ((u32)fidx<W>(tid, e, f0) >> (LOGN - s));
-                Lz.bfly(v[e], v[e2], __ldg(M.tw + g));
+                Lz.bfly(v[e], v[e | (1 << b)], tw[e >> (b + 1)]);
             }
         }
         if (CANON && p == NP - 1) {
@@ -198,12 +217,12 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
                     if (!(e & (1 << b))) Lz.last(v[e], v[e | (1 << b)], M);
                 continue;
             }
+            ulonglong2 tw[E / 2];
+            fetch_tw(tw, M.itw + (u32)h + ((u32)fidx<W>(tid, 0, f0) >> (lt + 1)), E >> (b + 1));
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
-                const int e2 = e | (1 << b);
-                const u32 g = (u32)h + ((u32)fidx<W>(tid, e, f0) >> (lt + 1));
-                Lz.bfly(v[e], v[e2], __ldg(M.itw + g));
+                Lz.bfly(v[e], v[e | (1 << b)], tw[e >> (b + 1)]);
             }
             if (Lz.red) {
 #pragma unroll
