@@ -293,11 +293,12 @@ DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo
             for (int e = 0; e < E; e++)
                 if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
         }
+        ulonglong2 tw[E / 2];
+        fetch_tw(tw, M.tw + (1 << s), E >> (b + 1));
 #pragma unroll
         for (int e = 0; e < E; e++) {
             if (e & (1 << b)) continue;
-            const int e2 = e | (1 << b);
-            Lz.bfly(v[e], v[e2], __ldg(M.tw + (1 << s) + (e >> (W - s))));
+            Lz.bfly(v[e], v[e | (1 << b)], tw[e >> (b + 1)]);
         }
     }
     cl.sync();   // every CTA of the cluster is resident before remote stores
@@ -330,12 +331,13 @@ DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo
                 for (int e = 0; e < E; e++)
                     if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
             }
+            ulonglong2 tw[E / 2];
+            fetch_tw(tw, M.tw + (1u << (sl + CL)) + ((u32)rank << sl) + ((u32)fidx<W>(tid, 0, f0) >> (LOGL - sl)),
+                     E >> (b + 1));
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
-                const int e2 = e | (1 << b);
-                const u32 g = (1u << (sl + CL)) + ((u32)rank << sl) + ((u32)fidx<W>(tid, e, f0) >> (LOGL - sl));
-                Lz.bfly(v[e], v[e2], __ldg(M.tw + g));
+                Lz.bfly(v[e], v[e | (1 << b)], tw[e >> (b + 1)]);
             }
         }
         if (CANON && p == NP - 1) {
@@ -374,12 +376,13 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
             const int lt = lt0 + ls;
             const int b = lt - f0;
             Lz.stage();
+            ulonglong2 tw[E / 2];
+            fetch_tw(tw, M.itw + (u32)(N >> (lt + 1)) + ((u32)rank << (LOGL - lt - 1)) + ((u32)fidx<W>(tid, 0, f0) >> (lt + 1)),
+                     E >> (b + 1));
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
-                const int e2 = e | (1 << b);
-                const u32 g = (u32)(N >> (lt + 1)) + ((u32)rank << (LOGL - lt - 1)) + ((u32)fidx<W>(tid, e, f0) >> (lt + 1));
-                Lz.bfly(v[e], v[e2], __ldg(M.itw + g));
+                Lz.bfly(v[e], v[e | (1 << b)], tw[e >> (b + 1)]);
             }
             if (Lz.red) {
 #pragma unroll
@@ -410,11 +413,12 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
                 if (!(e & (1 << b))) Lz.last(v[e], v[e | (1 << b)], M);
             continue;
         }
+        ulonglong2 tw[E / 2];
+        fetch_tw(tw, M.itw + (N >> (lt + 1)), E >> (b + 1));
 #pragma unroll
         for (int e = 0; e < E; e++) {
             if (e & (1 << b)) continue;
-            const int e2 = e | (1 << b);
-            Lz.bfly(v[e], v[e2], __ldg(M.itw + (N >> (lt + 1)) + (e >> (b + 1))));
+            Lz.bfly(v[e], v[e | (1 << b)], tw[e >> (b + 1)]);
         }
         if (Lz.red) {
 #pragma unroll
