@@ -238,11 +238,11 @@ static inline long long nblocks(long long total, int bs = 256) {
 static std::mutex g_attr_mu;
 static std::unordered_set<const void *> g_attr_done;
 
-template <int LOGN, bool INV = false, typename... KArgs, typename... Args>
+template <int LOGN, bool INV = false, int WO = 0, typename... KArgs, typename... Args>
 static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim3 grid, cudaStream_t st,
                        Args... args) {
     ProfScope ps_(c, name);
-    using C = RowCfg<LOGN, INV>;
+    using C = RowCfg<LOGN, INV, WO>;
     const size_t smem = (size_t)C::SMEM_WORDS * sizeof(u64);
     c->alg_mm += (double)grid.x * grid.y * grid.z * (C::N / 2) * LOGN;      // one (I)NTT per row
     {
@@ -295,7 +295,7 @@ static void launch_row(fhe_ctx *c, const char *name, void (*kern)(KArgs...), dim
 
 static int ntt_rows(fhe_ctx *c, int rows, const NttRowsArgs &a, const char *name = "k_ntt_rows") {
     if (rows <= 0) return 0;
-    LOGN_SWITCH(c->logn, launch_row<LG>(c, name, k_ntt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
+    LOGN_SWITCH(c->logn, launch_row<LG, false, FwdW5<LG>::value>(c, name, k_ntt_rows<LG>, dim3(rows), c->st, a, c->d_mods));
     CHECK_LAUNCH();
     return 0;
 }
@@ -1242,7 +1242,7 @@ struct KsOut {
 // ModUp: every off-diagonal (digit, prime) pair of S cts into Ext
 static int keyswitch_modup(fhe_ctx *c, int S, u32 l, const DigitTab &dt) {
     c->alg_mm -= (double)S * l * (c->n / 2) * c->logn;      // the diagonal rows return at once
-    LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_modup", k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
+    LOGN_SWITCH(c->logn, launch_row<LG, false, FwdW5<LG>::value>(c, "k_modup", k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
                                         c->d_mods));
     CHECK_LAUNCH();
     return 0;

@@ -66,8 +66,8 @@ struct NttRowsArgs {
 DEV long long row_off(int r, u32 rdiv, long long A, long long B) { return (long long)(r / rdiv) * A + (long long)(r % rdiv) * B; }
 
 template <int LOGN>
-__global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_ntt_rows(NttRowsArgs a, const ModInfo *__restrict__ mods) {
-    using C = RowCfg<LOGN, false>;
+__global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k_ntt_rows(NttRowsArgs a, const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false, FwdW5<LOGN>::value>;
     extern __shared__ u64 sm[];
     const int r = C::row(), tid = threadIdx.x, base = C::base();
     const ModInfo M = mods[a.map.id[(r / a.div) % a.period]];
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_ntt_rows(NttRowsArg
         else if (a.load == 2) x = centered_lift_lazy(x, half_src, msrc_q, M);
         v[e] = x;
     }
-    ntt_fwd_row<LOGN>(v, sm, M, tid);
+    ntt_fwd_row<LOGN, true, FwdW5<LOGN>::value>(v, sm, M, tid);
     u64 *dst = a.dst + row_off(r, a.rdiv, a.dA, a.dB) + base;
     for (int i = tid; i < C::NL; i += C::TH) {
         u64 x = sm[C::pad(i)];
@@ -194,9 +194,9 @@ struct DigitTab {
 // into prime i (i == l: the special prime) and transformed; the diagonal i == j is
 // skipped (the inner product reads it from DigitTab.ntt).
 template <int LOGN>
-__global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
+__global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
                                                              const ModInfo *__restrict__ mods) {
-    using C = RowCfg<LOGN, false>;
+    using C = RowCfg<LOGN, false, FwdW5<LOGN>::value>;
     extern __shared__ u64 sm[];
     const int s = C::row(), j = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
     if (i == j) return;
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_modup(DigitTab dt, 
     // centered lift: sign-symmetric, so it commutes with automorphisms (hoisted rotations)
 #pragma unroll
     for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(src[C::io(tid, e)], half_j, qj_mod, M);
-    const int B = ntt_fwd_row<LOGN, false>(v, sm, M, tid);
+    const int B = ntt_fwd_row<LOGN, false, FwdW5<LOGN>::value>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
     // the inner product accepts lazy digits while (l + 2) B q < 2^64 (its 128-bit sums of
     // l digit terms and up to two addend terms stay below q 2^64, the Montgomery bound)

@@ -255,12 +255,14 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
 #ifndef NTT_LOGL
 #define NTT_LOGL 14      // rows up to 2^NTT_LOGL words run on one CTA
 #endif
-template <int LOGN, bool INV>
+// WO != 0 overrides the radix of single-CTA rows (k_modup and k_ntt_rows run radix-32
+// forward passes: they are faster there, k_rescale is not -- DESIGN.md section 5)
+template <int LOGN, bool INV, int WO = 0>
 struct RowCfg {
     static constexpr int LOGL = LOGN > 14 ? 14 : (LOGN > NTT_LOGL ? NTT_LOGL : LOGN);    // log2 words per CTA
     static constexpr int CL = LOGN - LOGL;                // log2 CTAs per row
     static constexpr int CR = 1 << CL;
-    using Loc = NttCfg<LOGL, INV ? DefaultWInv<LOGL>::value : DefaultW<LOGL>::value>;
+    using Loc = NttCfg<LOGL, (WO && CL == 0) ? WO : (INV ? DefaultWInv<LOGL>::value : DefaultW<LOGL>::value)>;
     static constexpr int W = Loc::W, E = Loc::E, TH = Loc::TH, NL = Loc::N, N = 1 << LOGN;
     static constexpr int SMEM_WORDS = Loc::SMEM_WORDS;
     static_assert(CL <= 2 && CL <= W, "rows up to 2^16 words");
@@ -430,11 +432,19 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
 }
 
 // Row-size dispatch used by the row kernels.
-template <int LOGN, bool CANON = true>
-DEV int ntt_fwd_row(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo &M, int tid) {
-    if constexpr (RowCfg<LOGN, false>::CL == 0) return ntt_fwd_core<LOGN, DefaultW<LOGN>::value, CANON>(v, sm, M, tid);
+template <int LOGN, bool CANON = true, int WO = 0>
+DEV int ntt_fwd_row(u64 (&v)[RowCfg<LOGN, false, WO>::E], u64 *sm, const ModInfo &M, int tid) {
+    if constexpr (RowCfg<LOGN, false, WO>::CL == 0)
+        return ntt_fwd_core<LOGN, RowCfg<LOGN, false, WO>::W, CANON>(v, sm, M, tid);
     else return ntt_fwd_cluster<LOGN, CANON>(v, sm, M, tid);
 }
+#ifndef NTT_W_FUSED_FWD
+#define NTT_W_FUSED_FWD 5
+#endif
+template <int LOGN>
+struct FwdW5 {       // radix override for k_modup / k_ntt_rows
+    static constexpr int value = LOGN >= 12 ? NTT_W_FUSED_FWD : 0;
+};
 template <int LOGN>
 DEV void ntt_inv_row(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo &M, int tid) {
     if constexpr (RowCfg<LOGN, true>::CL == 0) ntt_inv_core<LOGN>(v, sm, M, tid);
