@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_intt_rows(InttRowsAr
     const u64 *src = a.src + row_off(r, a.rdiv, a.sA, a.sB);
     if (a.gather == 2 && C::CL == 0) {
         // single-CTA row: stage, then permute inside shared memory
-        for (int i = tid; i < C::NL; i += C::TH) sm[C::pad(i)] = src[i];
+        #pragma unroll
+        for (int i = tid, e_ = 0; e_ < C::E; i += C::TH, e_++) sm[C::pad(i)] = src[i];
         __syncthreads();
         u64 w[C::E];
 #pragma unroll
@@ -129,7 +130,8 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_intt_rows(InttRowsAr
 #pragma unroll
         for (int e = 0; e < C::E; e++) sm[C::pad(tid + e * C::TH)] = w[e];
     } else {
-        for (int i = tid; i < C::NL; i += C::TH) {
+        #pragma unroll
+        for (int i = tid, e_ = 0; e_ < C::E; i += C::TH, e_++) {
             const int gi = base + i;
             u64 x = a.gather == 1 ? src[a.tab[gi]] : a.gather == 2 ? src[galois_perm(gi, a.g, LOGN)] : src[gi];
             if (a.reduce) x = red64(x, M.q, M.mu);
@@ -166,12 +168,14 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_rot_gather_intt(PtrT
     const ModInfo M = mods[i];
     u64 v[C::E];
     if constexpr (C::CL == 0) {
-        for (int x = tid; x < C::NL; x += C::TH) sm[C::pad(x)] = src[x];
+        #pragma unroll
+        for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) sm[C::pad(x)] = src[x];
         __syncthreads();
         ntt_inv_core<LOGN>(v, sm, M, tid, g);
     } else {
         // cluster row: the automorphism gathers across CTAs, so read it from global memory
-        for (int x = tid; x < C::NL; x += C::TH) sm[C::pad(x)] = src[galois_perm(base + x, g, LOGN)];
+        #pragma unroll
+        for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) sm[C::pad(x)] = src[galois_perm(base + x, g, LOGN)];
         __syncthreads();
         ntt_inv_row<LOGN>(v, sm, M, tid);
     }
@@ -276,7 +280,8 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_rescale(RescaleArgs
     if (add && add_g) {
         if constexpr (C::CL == 0) {
             __syncthreads();
-            for (int x = tid; x < C::NL; x += C::TH) sm[C::pad(x)] = add[x];
+            #pragma unroll
+            for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) sm[C::pad(x)] = add[x];
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < C::E; e++) {
@@ -807,7 +812,8 @@ __global__ void __launch_bounds__(NttCfg<LOGN, W>::TH) k_bench_inv(const u64 *in
     const int tid = threadIdx.x;
     const ModInfo M = mods[mid];
     const u64 *src = in + (long long)blockIdx.x * C::N;
-    for (int i = tid; i < C::N; i += C::TH) sm[C::pad(i)] = src[i];
+    #pragma unroll
+    for (int i = tid, e_ = 0; e_ < C::E; i += C::TH, e_++) sm[C::pad(i)] = src[i];
     __syncthreads();
     u64 v[C::E];
     ntt_inv_core<LOGN, W>(v, sm, M, tid);
