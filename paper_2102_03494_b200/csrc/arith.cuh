@@ -81,10 +81,11 @@ DEV u64 mont_reduce(u64 hi, u64 lo, u64 q, u64 qinv) {
     u64 mh = mulhi(m, q);
     return hi >= mh ? hi - mh : hi - mh + q;
 }
-DEV void mac128(u64 &hi, u64 &lo, u64 a, u64 b) {      // (hi, lo) += a * b
-    u64 pl = a * b, ph = mulhi(a, b);
-    lo += pl;
-    hi += ph + (lo < pl ? 1 : 0);
+DEV void mac128(u64 &hi, u64 &lo, u64 a, u64 b) {      // (hi, lo) += a * b (exact, carry chained)
+    asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\t"
+        "madc.hi.u64 %1, %2, %3, %1;"
+        : "+l"(lo), "+l"(hi)
+        : "l"(a), "l"(b));
 }
 DEV u64 addm(u64 a, u64 b, u64 q) { u64 s = a + b; return s >= q ? s - q : s; }
 DEV u64 subm(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }

@@ -337,23 +337,28 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
                                                      int S, int L, int logn, int special_id,
                                                      const ModInfo *__restrict__ mods, const KsAdd ka_) {
     constexpr int l = LL;
-    const long long n = 1ll << logn;
-    const int groups = (S + KS_GROUP - 1) / KS_GROUP;
-    GRID_STRIDE(idx, (long long)groups * (l + 1) * n) {
-        const long long x = idx & (n - 1);
-        const long long r = idx >> logn;
+    // 32-bit index math: workspace offsets stay below 2^32 words (a few GB at most)
+    const u32 n = 1u << logn;
+    const u32 groups = (S + KS_GROUP - 1) / KS_GROUP;
+    const u32 total = groups * (l + 1) * n;
+    const u32 estride = (l + 1) * n;                    // Ext: digit j -> j + 1
+    const u32 kstride = 2u * (L + 1) * n;               // key: digit j -> j + 1
+    for (u32 idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const u32 x = idx & (n - 1);
+        const u32 r = idx >> logn;
         const int i = (int)(r % (l + 1));
         const int s0 = KS_GROUP * (int)(r / (l + 1));
         const int kp = i == l ? L : i;
         const ModInfo &M = mods[i == l ? special_id : i];
         const u64 q = M.q, qi = M.qinv;
+        const u32 kb0 = (u32)kp * n + x, ka0 = (u32)(L + 1 + kp) * n + x;
         u64 kb[l], ka[l];
         const int sc = S - s0 < KS_GROUP ? S - s0 : KS_GROUP;
         const u64 *cur = dt.key[s0];
 #pragma unroll
         for (int j = 0; j < l; j++) {
-            kb[j] = __ldg(cur + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
-            ka[j] = __ldg(cur + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
+            kb[j] = __ldg(cur + j * kstride + kb0);
+            ka[j] = __ldg(cur + j * kstride + ka0);
         }
         for (int u = 0; u < sc; u++) {
             const int s = s0 + u;
@@ -361,18 +366,19 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
                 cur = dt.key[s];
 #pragma unroll
                 for (int j = 0; j < l; j++) {
-                    kb[j] = __ldg(cur + (((long long)j * 2 + 0) * (L + 1) + kp) * n + x);
-                    ka[j] = __ldg(cur + (((long long)j * 2 + 1) * (L + 1) + kp) * n + x);
+                    kb[j] = __ldg(cur + j * kstride + kb0);
+                    ka[j] = __ldg(cur + j * kstride + ka0);
                 }
             }
             // hoisted rotations share one ModUp: Ext(tau_g(c1)) = Ext(c1) read at perm_g(x)
-            const long long xs = dt.perm[s] ? (long long)galois_perm((u32)x, dt.perm[s], logn) : x;
-            const long long xd = dt.dperm[s] ? (long long)galois_perm((u32)x, dt.dperm[s], logn) : x;
-            const int es = dt.perm[s] ? (int)dt.esrc[s] : s;
+            const u32 xs = dt.perm[s] ? galois_perm(x, dt.perm[s], logn) : x;
+            const u32 xd = dt.dperm[s] ? galois_perm(x, dt.dperm[s], logn) : x;
+            const u32 es = dt.perm[s] ? dt.esrc[s] : (u32)s;
+            const u64 *eb = Ext + (es * l * (l + 1) + i) * n + xs;
+            const u64 *db = dt.ntt[s] + xd;
             u64 e[l];
 #pragma unroll
-            for (int j = 0; j < l; j++)
-                e[j] = i == j ? dt.ntt[s][(long long)j * n + xd] : Ext[((((long long)es * l + j) * (l + 1)) + i) * n + xs];
+            for (int j = 0; j < l; j++) e[j] = i == j ? db[j * n] : eb[j * estride];
             u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
 #pragma unroll
             for (int j = 0; j < l; j++) {
@@ -382,17 +388,18 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
             if (i < l) {
                 const u64 pr = ka_.pr[i];
                 if (const u64 *ad = ka_.add[s]) {
-                    const long long xa = ka_.add_g[s] ? (long long)galois_perm((u32)x, ka_.add_g[s], logn) : x;
-                    if (ka_.add_pmask & 1) mac128(h0, l0, ad[(long long)i * n + xa], pr);
-                    if (ka_.add_pmask & 2) mac128(h1, l1, ad[ka_.add_pstride + (long long)i * n + xa], pr);
+                    const u32 xa = ka_.add_g[s] ? galois_perm(x, ka_.add_g[s], logn) : x;
+                    if (ka_.add_pmask & 1) mac128(h0, l0, ad[(u32)i * n + xa], pr);
+                    if (ka_.add_pmask & 2) mac128(h1, l1, ad[ka_.add_pstride + (u32)i * n + xa], pr);
                 }
                 if (const u64 *ac = ka_.acc[s]) {
-                    mac128(h0, l0, ac[(long long)i * n + x], pr);
-                    mac128(h1, l1, ac[ka_.acc_pstride + (long long)i * n + x], pr);
+                    mac128(h0, l0, ac[(u32)i * n + x], pr);
+                    mac128(h1, l1, ac[ka_.acc_pstride + (u32)i * n + x], pr);
                 }
             }
-            Acc[(((long long)s * 2 + 0) * (l + 1) + i) * n + x] = mont_reduce(h0, l0, q, qi);
-            Acc[(((long long)s * 2 + 1) * (l + 1) + i) * n + x] = mont_reduce(h1, l1, q, qi);
+            u64 *ob = Acc + ((u32)s * 2 * (l + 1) + i) * n + x;
+            ob[0] = mont_reduce(h0, l0, q, qi);
+            ob[estride] = mont_reduce(h1, l1, q, qi);
         }
     }
 }
