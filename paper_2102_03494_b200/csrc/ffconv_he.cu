@@ -1317,7 +1317,7 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     }
     ra.src_id = c->special_id;
     for (u32 i = 0; i < l; i++) { ra.fac[i] = c->pinv[i]; ra.fac_sh[i] = c->pinv_sh[i]; }
-    LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
+    LOGN_SWITCH(c->logn, launch_row<LG, false, RescaleW<LG>::value>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
     CHECK_LAUNCH();
     return 0;
 }
@@ -1592,7 +1592,7 @@ extern "C" int fhe_mod_switch(fhe_ctx *c, const fhe_ct *a, fhe_ct *out) {
         ra.out_pstride = (long long)(l - 1) * n;
         ra.src_id = (int)(l - 1);
         for (u32 i = 0; i + 1 < l; i++) { ra.fac[i] = T.msinv[i]; ra.fac_sh[i] = T.msinv_sh[i]; }
-        LOGN_SWITCH(c->logn, launch_row<LG>(c, "k_rescale(modswitch)", k_rescale<LG>, dim3(S, 2, l - 1), c->st, ra, c->d_mods));
+        LOGN_SWITCH(c->logn, launch_row<LG, false, RescaleW<LG>::value>(c, "k_rescale(modswitch)", k_rescale<LG>, dim3(S, 2, l - 1), c->st, ra, c->d_mods));
         CHECK_LAUNCH();
     }
     return 0;

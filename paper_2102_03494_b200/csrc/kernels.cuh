@@ -242,9 +242,16 @@ struct RescaleArgs {
     u64 fac[MAXQ], fac_sh[MAXQ];
 };
 
+#ifndef NTT_W_RESCALE
+#define NTT_W_RESCALE 0      // 0: the default forward radix
+#endif
 template <int LOGN>
-__global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
-    using C = RowCfg<LOGN, false>;
+struct RescaleW {
+    static constexpr int value = LOGN >= 12 ? NTT_W_RESCALE : 0;
+};
+template <int LOGN>
+__global__ void __launch_bounds__(RowCfg<LOGN, false, RescaleW<LOGN>::value>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false, RescaleW<LOGN>::value>;
     extern __shared__ u64 sm[];
     const int s = C::row(), p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x, gb = C::base();
     const long long n = C::N;
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false>::TH) k_rescale(RescaleArgs
     u64 v[C::E];
 #pragma unroll
     for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(r[C::io(tid, e)], half_src, msrc_q, M);
-    const int B = ntt_fwd_row<LOGN, false>(v, sm, M, tid);
+    const int B = ntt_fwd_row<LOGN, false, RescaleW<LOGN>::value>(v, sm, M, tid);
     const u64 *base = a.base[s] + p * a.base_pstride + i * n + gb;
     u64 *out = a.out[s] + p * a.out_pstride + i * n + gb;
     const u64 *add = ((a.add_pmask >> p) & 1) && a.add[s] ? a.add[s] + p * a.add_pstride + i * n : nullptr;
