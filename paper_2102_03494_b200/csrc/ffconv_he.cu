@@ -161,12 +161,14 @@ struct fhe_ctx {
     u64 *enc_stage[2]{};
     cudaEvent_t enc_ev[2]{};
     int enc_next = 0;
-    // workspaces (key switching: two ping-pong sets, one per stream)
+    // workspaces (key switching: one set per lane; lanes = streams the sub-batches rotate over)
     int S = 1;                          // key-switching sub-batch
     u64 *w_D = nullptr, *w_Ext = nullptr, *w_Acc = nullptr;   // current set
-    u64 *ws_D[2]{}, *ws_Ext[2]{}, *ws_Acc[2]{};
-    cudaStream_t streams[2]{};
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_key = nullptr;
+    static constexpr int MAXLANES = 4;
+    int lanes = 2;                      // FHE_LANES (1..4)
+    u64 *ws_D[MAXLANES]{}, *ws_Ext[MAXLANES]{}, *ws_Acc[MAXLANES]{};
+    cudaStream_t streams[MAXLANES]{};
+    cudaEvent_t ev_fork = nullptr, ev_key = nullptr, ev_join[MAXLANES]{};
     u64 *w_sq = nullptr;
     size_t w_sq_words = 0;
     u64 *w_tmp = nullptr;
@@ -546,15 +548,19 @@ static int setup_workspace(fhe_ctx *c) {
     if (S < 1) S = 1;
     if (S > MAXS) S = MAXS;
     c->S = S;
-    for (int k = 0; k < 2; k++) {
+    const char *lenv = getenv("FHE_LANES");
+    c->lanes = lenv ? std::max(1, std::min(fhe_ctx::MAXLANES, atoi(lenv))) : 2;
+    for (int k = 0; k < c->lanes; k++) {
         CU(cudaMalloc((void **)&c->ws_D[k], S * L * n * 8));
         CU(cudaMalloc((void **)&c->ws_Ext[k], S * L * (L + 1) * n * 8));
         CU(cudaMalloc((void **)&c->ws_Acc[k], S * 2 * (L + 1) * n * 8));
     }
     c->w_D = c->ws_D[0]; c->w_Ext = c->ws_Ext[0]; c->w_Acc = c->ws_Acc[0];
-    CU(cudaStreamCreateWithFlags(&c->streams[1], cudaStreamNonBlocking));
+    for (int k = 1; k < c->lanes; k++) {
+        CU(cudaStreamCreateWithFlags(&c->streams[k], cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));
+    }
     CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&c->ev_key, cudaEventDisableTiming));
     CU(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
@@ -658,13 +664,15 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
     void *bufs[] = {c->d_mods, c->d_tw, c->d_s_can, c->d_s_m, c->d_s2_m, c->d_sk_ids, c->d_slot2ntt,
                     c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_sq};
     for (void *b : bufs) if (b) cudaFree(b);
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < fhe_ctx::MAXLANES; k++) {
         void *wb[] = {c->ws_D[k], c->ws_Ext[k], c->ws_Acc[k]};
         for (void *b : wb) if (b) cudaFree(b);
     }
-    if (c->streams[1]) { cudaStreamSynchronize(c->streams[1]); cudaStreamDestroy(c->streams[1]); }
+    for (int k = 1; k < fhe_ctx::MAXLANES; k++) {
+        if (c->streams[k]) { cudaStreamSynchronize(c->streams[k]); cudaStreamDestroy(c->streams[k]); }
+        if (c->ev_join[k]) cudaEventDestroy(c->ev_join[k]);
+    }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_key) cudaEventDestroy(c->ev_key);
     if (c->w_tmp) cudaFreeAsync(c->w_tmp, c->st);
     if (c->st) { cudaStreamSynchronize(c->st); cudaStreamDestroy(c->st); }
@@ -911,7 +919,7 @@ static int get_key(fhe_ctx *c, u32 kid, const u64 **out) {
         CU(cudaMalloc((void **)&kb.d, words * 8));
     }
     kb.last = c->key_tick;
-    // generate on stream 0 (the shared w_tmp lives there); the other lane waits for it
+    // generate on stream 0 (the shared w_tmp lives there); the other lanes wait for it
     cudaStream_t caller = c->st;
     c->st = c->streams[0];
     TRY(ensure_tmp(c, L * (L + 1) * n));
@@ -926,11 +934,11 @@ static int get_key(fhe_ctx *c, u32 kid, const u64 **out) {
        (int)c->logn, c->P.seed, kid, c->special_id, c->d_mods);
     CHECK_LAUNCH();
     c->st = caller;
-    if (c->streams[1]) {
-        // every later launch on the other lane (not only the caller's: a cached key is
+    if (c->lanes > 1) {
+        // every later launch on the other lanes (not only the caller's: a cached key is
         // reused by the next sub-batch without a wait) is ordered after the generation
         CU(cudaEventRecord(c->ev_key, c->streams[0]));
-        CU(cudaStreamWaitEvent(c->streams[1], c->ev_key, 0));
+        for (int k = 1; k < c->lanes; k++) CU(cudaStreamWaitEvent(c->streams[k], c->ev_key, 0));
     }
     c->keys[kid] = kb;
     c->key_bytes += words * 8;
@@ -1342,17 +1350,17 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
     std::vector<const u64 *> keys(in.size());
     size_t n = c->n;
     // (profiling runs single-stream so every kernel is timed in isolation)
-    const bool two = in.size() > (size_t)c->S && !c->prof;
+    const bool two = in.size() > (size_t)c->S && !c->prof && c->lanes > 1;
     // balanced sub-batches: ceil(count / ceil(count / S)) instead of S + remainder
     const size_t nsub = (in.size() + c->S - 1) / c->S;
     const size_t SB = (in.size() + nsub - 1) / nsub;
     if (two) {
         CU(cudaEventRecord(c->ev_fork, c->streams[0]));
-        CU(cudaStreamWaitEvent(c->streams[1], c->ev_fork, 0));
+        for (int k = 1; k < c->lanes; k++) CU(cudaStreamWaitEvent(c->streams[k], c->ev_fork, 0));
     }
     int rc = 0;
     int lane = 0;
-    for (size_t b0 = 0; b0 < in.size() && !rc; b0 += SB, lane ^= 1) {
+    for (size_t b0 = 0; b0 < in.size() && !rc; b0 += SB, lane = (lane + 1) % c->lanes) {
         use_lane(c, two ? lane : 0);
         int S = (int)std::min<size_t>(SB, in.size() - b0);
         c->key_tick++;                       // keys of this sub-batch are pinned
@@ -1389,8 +1397,10 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
     }
     use_lane(c, 0);
     if (two) {
-        CU(cudaEventRecord(c->ev_join, c->streams[1]));
-        CU(cudaStreamWaitEvent(c->streams[0], c->ev_join, 0));
+        for (int k = 1; k < c->lanes; k++) {
+            CU(cudaEventRecord(c->ev_join[k], c->streams[k]));
+            CU(cudaStreamWaitEvent(c->streams[0], c->ev_join[k], 0));
+        }
     }
     return rc;
 }
