@@ -1113,12 +1113,16 @@ extern "C" int fhe_encrypt(fhe_ctx *c, const uint64_t *slots, uint32_t nonce, fh
 // x = INTT(c0 + c1 s) into dst [count][l][n]
 static int raw_decrypt(fhe_ctx *c, const fhe_ct *ct, u64 *dst) {
     size_t n = c->n, l = ct->level;
-    long long total = (long long)ct->count * l * n;
-    EW(k_dec_mul, total, ct->d, c->d_s_m, dst, total, (int)l, (int)c->logn, c->d_mods);
-    CHECK_LAUNCH();
-    InttRowsArgs a = iargs(dst, dst, n);
+    // row r = (ci, i): c0 + c1 s computed while staging the inverse NTT (gather mode 3)
+    InttRowsArgs a = iargs(ct->d, dst, n);
+    a.rdiv = (u32)l;
+    a.sA = (long long)2 * l * n; a.sB = (long long)n;
+    a.dA = (long long)l * n; a.dB = (long long)n;
     a.period = l;
     map_q(a.map, l);
+    a.gather = 3;
+    a.c1off = (long long)l * n;
+    a.s_m = c->d_s_m;
     return intt_rows(c, (int)(ct->count * l), a);
 }
 

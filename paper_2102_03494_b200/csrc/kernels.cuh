@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k
 
 // Inverse NTT of rows, optional gather on load:
 //   gather 0: none   1: src[tab[j]] (slot -> NTT position)   2: automorphism by g
+//   3: decryption, c0 + c1 * s (c1 at src + c1off, s in Montgomery form per prime)
 struct InttRowsArgs {
     const u64 *src;
     u64 *dst;
@@ -109,6 +110,8 @@ struct InttRowsArgs {
     const u32 *tab;
     u32 g;
     int reduce;   // 1: reduce inputs mod q first (values may exceed q)
+    long long c1off;
+    const u64 *s_m;
 };
 
 template <int LOGN>
@@ -116,9 +119,17 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_intt_rows(InttRowsAr
     using C = RowCfg<LOGN, true>;
     extern __shared__ u64 sm[];
     const int r = C::row(), tid = threadIdx.x, base = C::base();
-    const ModInfo M = mods[a.map.id[(r / a.div) % a.period]];
+    const int mid = a.map.id[(r / a.div) % a.period];
+    const ModInfo M = mods[mid];
     const u64 *src = a.src + row_off(r, a.rdiv, a.sA, a.sB);
-    if (a.gather == 2 && C::CL == 0) {
+    if (a.gather == 3) {
+        const u64 *c1 = src + a.c1off, *sk = a.s_m + (long long)mid * C::N;
+#pragma unroll
+        for (int i = tid, e_ = 0; e_ < C::E; i += C::TH, e_++) {
+            const int gi = base + i;
+            sm[C::pad(i)] = addm(src[gi], mont(c1[gi], sk[gi], M.q, M.qinv), M.q);
+        }
+    } else if (a.gather == 2 && C::CL == 0) {
         // single-CTA row: stage, then permute inside shared memory
         #pragma unroll
         for (int i = tid, e_ = 0; e_ < C::E; i += C::TH, e_++) sm[C::pad(i)] = src[i];
