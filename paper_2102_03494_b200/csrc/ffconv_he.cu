@@ -1099,13 +1099,19 @@ extern "C" int fhe_encrypt(fhe_ctx *c, const uint64_t *slots, uint32_t nonce, fh
     EW(k_enc_prep, total8, m, tmp, total8, (int)L, (int)ct->R, (int)c->logn, c->P.seed, nonce, c->d_lv + L, c->t_id0,
        c->d_mods);
     CHECK_LAUNCH();
-    NttRowsArgs a = nargs(tmp, tmp, n);
+    // NTT of every (ci, i) row, the uniform a and c0 = v - a s in its epilogue (epi 3)
+    NttRowsArgs a = nargs(tmp, ct->d, n);
     a.period = L;
     map_q(a.map, L);
+    a.rdiv = (u32)L;
+    a.sA = (long long)L * n; a.sB = (long long)n;
+    a.dA = (long long)2 * L * n; a.dB = (long long)n;
+    a.epi = 3;
+    a.seed = c->P.seed;
+    a.nonce = nonce;
+    a.s_m = c->d_s_m;
+    a.c1off = (long long)L * n;
     TRY(ntt_rows(c, (int)(cnt * L), a));
-    const long long total4 = (long long)cnt * L * ((n + 3) / 4);
-    EW(k_enc_finish, total4, tmp, ct->d, c->d_s_m, total4, (int)L, (int)c->logn, c->P.seed, nonce, c->d_mods);
-    CHECK_LAUNCH();
     if (!async) CU(cudaStreamSynchronize(c->st));      // pageable input: the host buffer may be reused
     return 0;
 }

@@ -53,6 +53,8 @@ struct ModMap {
 //   load 0: plain (< 4q)   1: reduce any 64-bit word   2: centered lift from
 //           source modulus srcmap (values in [0, m_src))
 //   epi  0: store canonical   1: store Montgomery form   2: dst += v
+//        3: encryption, row r = (ci, i): c1 = a (uniform, ChaCha20 as in k_enc_finish),
+//           c0 = v - a s, with c0 at dst and c1 at dst + c1off
 struct NttRowsArgs {
     const u64 *src;
     u64 *dst;
@@ -62,6 +64,10 @@ struct NttRowsArgs {
     u32 div2, period2;             // source modulus: srcmap.id[(r / div2) % period2]
     ModMap map, srcmap;
     int load, epi;
+    u64 seed;                      // epi 3
+    u32 nonce;
+    const u64 *s_m;
+    long long c1off;
 };
 DEV long long row_off(int r, u32 rdiv, long long A, long long B) { return (long long)(r / rdiv) * A + (long long)(r % rdiv) * B; }
 
@@ -88,6 +94,26 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k
     }
     ntt_fwd_row<LOGN, true, FwdW5<LOGN>::value>(v, sm, M, tid);
     u64 *dst = a.dst + row_off(r, a.rdiv, a.dA, a.dB) + base;
+    if (a.epi == 3) {
+        // four consecutive coefficients per ChaCha20 block: one block per thread and group
+        const int mid = a.map.id[(r / a.div) % a.period];
+        const u32 ci = (u32)r / a.rdiv, li = (u32)r % a.rdiv;
+        const u64 *sk = a.s_m + (long long)mid * C::N + base;
+        for (int g = tid; g < C::NL / 4; g += C::TH) {
+            u32 blk[16];
+            chacha_block(blk, a.seed, (u32)(base + 4 * g) >> 2, DOM_ENC_A, li, a.nonce, ci);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int i = 4 * g + u;
+                const u128 w = ((u128)blk[4 * u + 3] << 96) | ((u128)blk[4 * u + 2] << 64) |
+                               ((u128)blk[4 * u + 1] << 32) | blk[4 * u];
+                const u64 av = mod128(w, M);
+                dst[i] = subm(sm[C::pad(i)], mont(av, sk[i], M.q, M.qinv), M.q);
+                dst[a.c1off + i] = av;
+            }
+        }
+        return;
+    }
     for (int i = tid; i < C::NL; i += C::TH) {
         u64 x = sm[C::pad(i)];
         if (a.epi == 1) x = to_mont(x, M);
