@@ -113,8 +113,8 @@ def algorithmic_counts(n: int, l: int):
     return {
         "k_rot_gather_intt": (l * ntt, (2 * l * n + 2 * l * n + l * n) * w),
         "k_modup": (l * l * ntt, (l * l * n + l * l * n) * w),
-        "k_ks_inner": (2 * l * (l + 1) * n, (l * (l + 1) * n + 2 * (l + 1) * n) * w),
-        "k_intt_rows(moddown)": (2 * ntt, 4 * n * w),
+        "k_ks_inner": (2 * l * l * n, (l * l * n + 2 * l * n) * w),
+        "k_ks_special": (2 * ntt + 2 * l * n, (2 * l * n + 2 * n) * w),
         "k_rescale(moddown)": (2 * l * ntt + 2 * l * n, (2 * n + 2 * l * n + l * n + 2 * l * n) * w),
     }
 

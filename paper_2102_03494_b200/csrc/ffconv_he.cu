@@ -1276,7 +1276,7 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     if (ksv < 0) { const char *e = getenv("FHE_KS_VARIANT"); ksv = e ? atoi(e) : 2; }   // 2: measured best (4 cts/thread, 4 CTAs/SM)
     const int G = (ksv == 1 || ksv == 3) ? 2 : 4;
     c->alg_mm += (double)S * (2.0 * l * (l + 1) + 2.0 * l) * n;   // key inner product + ModDown scaling
-    long long tot = (long long)((S + G - 1) / G) * (l + 1) * n;
+    long long tot = (long long)((S + G - 1) / G) * l * n;
     // fold the addends into the inner product while its Montgomery input bound holds
     // ((l + 2) q_i < 2^64: l digit terms + 2 addend terms, each < q_i^2); else the
     // rescale epilogue adds them
@@ -1313,10 +1313,10 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
 #undef KS_LAUNCH
     }
     CHECK_LAUNCH();
-    // ModDown: INTT of the special limb of both accumulators
-    InttRowsArgs ia = iargs(c->w_Acc + l * n, c->w_Acc + l * n, (long long)(l + 1) * n);
-    ia.map.id[0] = (unsigned char)c->special_id;
-    TRY(intt_rows(c, 2 * S, ia, "k_intt_rows(moddown)"));
+    // the special prime's inner product + ModDown INTT of both accumulators (one row each)
+    LOGN_SWITCH(c->logn, launch_row<LG, true>(c, "k_ks_special", k_ks_special<LG>, dim3(2 * S), c->st,
+                                              (const u64 *)c->w_Ext, dt, c->w_Acc, (int)l, L, c->special_id, c->d_mods));
+    CHECK_LAUNCH();
     RescaleArgs ra;
     memset(&ra, 0, sizeof ra);
     for (int s = 0; s < S; s++) {

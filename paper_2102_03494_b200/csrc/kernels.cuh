@@ -384,16 +384,17 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
     // 32-bit index math: workspace offsets stay below 2^32 words (a few GB at most)
     const u32 n = 1u << logn;
     const u32 groups = (S + KS_GROUP - 1) / KS_GROUP;
-    const u32 total = groups * (l + 1) * n;
+    // the special prime's rows (i = l) are k_ks_special's: inner product + ModDown INTT
+    const u32 total = groups * l * n;
     const u32 estride = (l + 1) * n;                    // Ext: digit j -> j + 1
     const u32 kstride = 2u * (L + 1) * n;               // key: digit j -> j + 1
     for (u32 idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
         const u32 x = idx & (n - 1);
         const u32 r = idx >> logn;
-        const int i = (int)(r % (l + 1));
-        const int s0 = KS_GROUP * (int)(r / (l + 1));
-        const int kp = i == l ? L : i;
-        const ModInfo &M = mods[i == l ? special_id : i];
+        const int i = (int)(r % l);
+        const int s0 = KS_GROUP * (int)(r / l);
+        const int kp = i;
+        const ModInfo &M = mods[i];
         const u64 q = M.q, qi = M.qinv;
         const u32 kb0 = (u32)kp * n + x, ka0 = (u32)(L + 1 + kp) * n + x;
         u64 kb[l], ka[l];
@@ -429,7 +430,7 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
                 mac128(h0, l0, e[j], kb[j]);
                 mac128(h1, l1, e[j], ka[j]);
             }
-            if (i < l) {
+            {
                 const u64 pr = ka_.pr[i];
                 if (const u64 *ad = ka_.add[s]) {
                     const u32 xa = ka_.add_g[s] ? galois_perm(x, ka_.add_g[s], logn) : x;
@@ -446,6 +447,42 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
             ob[estride] = mont_reduce(h1, l1, q, qi);
         }
     }
+}
+
+// Key switching, the special prime's rows: grid 2S rows (s, p).  The inner product
+// acc = sum_j Ext[s][j][P] * key_p[j][P] is formed while staging the ModDown inverse NTT
+// (no accumulator round trip, and k_ks_inner only covers the q primes); the row is
+// left in coefficient form in Acc[s][p][l] for k_rescale.
+template <int LOGN>
+__global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_ks_special(const u64 *__restrict__ Ext, DigitTab dt, u64 *Acc,
+                                                                 int l, int L, int special_id,
+                                                                 const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, true>;
+    extern __shared__ u64 sm[];
+    const int r = C::row(), tid = threadIdx.x, base = C::base();
+    const int s = r >> 1, p = r & 1;
+    const u32 n = C::N;
+    const ModInfo M = mods[special_id];
+    const u64 *key = dt.key[s] + ((u32)p * (L + 1) + L) * n;
+    const u32 kstride = 2u * (L + 1) * n, estride = (l + 1) * n;
+    const u32 es = dt.perm[s] ? dt.esrc[s] : (u32)s;
+    const u64 *eb = Ext + (es * l * (l + 1) + l) * n;
+    const u32 g = dt.perm[s];
+#pragma unroll
+    for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) {
+        const u32 gx = base + x;
+        const u32 xs = g ? galois_perm(gx, g, LOGN) : gx;
+        u64 h = 0, lo = 0;
+#pragma unroll 4
+        for (int j = 0; j < l; j++) mac128(h, lo, eb[j * estride + xs], __ldg(key + j * kstride + gx));
+        sm[C::pad(x)] = mont_reduce(h, lo, M.q, M.qinv);
+    }
+    __syncthreads();
+    u64 v[C::E];
+    ntt_inv_row<LOGN>(v, sm, M, tid);
+    u64 *dst = Acc + ((u32)s * 2 * (l + 1) + (u32)p * (l + 1) + l) * n;
+#pragma unroll
+    for (int e = 0; e < C::E; e++) dst[C::io(tid, e)] = v[e];
 }
 
 // out = a + b over [count][2][l][n]
