@@ -119,6 +119,17 @@ def algorithmic_counts(n: int, l: int):
     }
 
 
+def kernel_counts(n: int, l: int):
+    """algorithmic_counts plus the fused ModDown (k_moddown = the q primes' inner
+    product + the ModDown rescale, the default path)."""
+    c = algorithmic_counts(n, l)
+    w = 8
+    ntt = (n // 2) * int(math.log2(n))
+    c["k_moddown"] = (c["k_ks_inner"][0] + c["k_rescale(moddown)"][0],
+                      (l * l * n + 2 * n + l * n + 2 * l * n) * w)
+    return c
+
+
 def rotation_modmuls(n, l):
     return sum(v[0] for v in algorithmic_counts(n, l).values())
 
@@ -258,7 +269,7 @@ def run_rotation(args, rank, world, local_rank):
     lib.call("fhe_prof_report", ev.ctx, buf, len(buf))
     lib.call("fhe_prof_enable", ev.ctx, 0)
     prof = parse_prof(buf.value.decode())
-    counts = algorithmic_counts(n, P.L)
+    counts = kernel_counts(n, P.L)
     steps_prof = max(1, args.steps)
     kern = {}
     for name, (calls, ms) in prof.items():

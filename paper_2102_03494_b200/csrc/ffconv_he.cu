@@ -1292,7 +1292,13 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
         kad.add_pmask = ko.add_pmask;
         for (u32 i = 0; i < l; i++) kad.pr[i] = c->pmont[i];
     }
-    {
+    // FHE_FUSED_MODDOWN=1: the q primes' inner product runs in k_moddown's epilogue instead
+    // of a separate k_ks_inner pass (needs the addend fold).  Off by default: measured 3 %
+    // slower (the epilogue serialises behind the NTT in each CTA)
+    static int fused_env = -1;
+    if (fused_env < 0) { const char *e = getenv("FHE_FUSED_MODDOWN"); fused_env = e ? atoi(e) : 0; }
+    const bool fused = fold && fused_env != 0;
+    if (!fused) {
         ProfScope ps_(c, "k_ks_inner");
         const unsigned nb = (unsigned)nblocks(tot);
 #define KS_LAUNCH(LLV, GV, MB) k_ks_inner<LLV, GV, MB><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, \
@@ -1335,7 +1341,12 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     }
     ra.src_id = c->special_id;
     for (u32 i = 0; i < l; i++) { ra.fac[i] = c->pinv[i]; ra.fac_sh[i] = c->pinv_sh[i]; }
-    LOGN_SWITCH(c->logn, launch_row<LG, false, RescaleW<LG>::value>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
+    if (fused) {
+        LOGN_SWITCH(c->logn, launch_row<LG, false, RescaleW<LG>::value>(c, "k_moddown", k_moddown<LG>, dim3(S, 2, l), c->st, ra,
+                                                                        (const u64 *)c->w_Ext, dt, kad, (int)l, L, c->d_mods));
+    } else {
+        LOGN_SWITCH(c->logn, launch_row<LG, false, RescaleW<LG>::value>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
+    }
     CHECK_LAUNCH();
     return 0;
 }

@@ -485,6 +485,57 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_ks_special(const u64
     for (int e = 0; e < C::E; e++) dst[C::io(tid, e)] = v[e];
 }
 
+// ModDown with the q primes' key inner product folded into its epilogue (no Ext re-read
+// by a separate pass, no accumulator round trip): grid (S, 2, l), row (s, p, i)
+//   out = (sum_j Ext[s][j][i] key_p[j][i] + addends (KsAdd) - NTT_i(lift(coef_p))) * P^-1
+// where coef_p is the special row k_ks_special left in coefficient form.
+template <int LOGN>
+__global__ void __launch_bounds__(RowCfg<LOGN, false, RescaleW<LOGN>::value>::TH)
+    k_moddown(RescaleArgs a, const u64 *__restrict__ Ext, DigitTab dt, KsAdd ka_, int l, int L,
+              const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false, RescaleW<LOGN>::value>;
+    extern __shared__ u64 sm[];
+    const int s = C::row(), p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x, gb = C::base();
+    const u32 n = C::N;
+    const ModInfo M = mods[i];
+    const ModInfo &S = mods[a.src_id];
+    const u64 half_src = S.half, msrc_q = red64(S.q, M.q, M.mu);
+    const u64 *r = a.coef[s] + p * a.coef_pstride;
+    u64 v[C::E];
+#pragma unroll
+    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(r[C::io(tid, e)], half_src, msrc_q, M);
+    const int B = ntt_fwd_row<LOGN, false, RescaleW<LOGN>::value>(v, sm, M, tid);
+    // inner-product operands of row (s, p, i)
+    const u32 kstride = 2u * (L + 1) * n, estride = (l + 1) * n;
+    const u64 *key = dt.key[s] + ((u32)p * (L + 1) + i) * n;
+    const u32 es = dt.perm[s] ? dt.esrc[s] : (u32)s;
+    const u64 *eb = Ext + (es * l * (l + 1) + i) * n;
+    const u64 *db = dt.ntt[s] + (u32)i * n;
+    const u32 gp = dt.perm[s], gd = dt.dperm[s], ga = ka_.add_g[s];
+    const u64 pr = ka_.pr[i];
+    const u64 *ad = ((ka_.add_pmask >> p) & 1) && ka_.add[s] ? ka_.add[s] + p * ka_.add_pstride + (u32)i * n : nullptr;
+    const u64 *ac = ka_.acc[s] ? ka_.acc[s] + p * ka_.acc_pstride + (u32)i * n : nullptr;
+    u64 *out = a.out[s] + p * a.out_pstride + (u32)i * n + gb;
+    const u64 f = a.fac[i], fsh = a.fac_sh[i];
+    const bool lazy = (u128)(B + 1) * M.q < ((u128)1 << 64);
+    const u64 Bq = (u64)B * M.q;
+#pragma unroll 4
+    for (int e = 0; e < C::E; e++) {
+        const int x = tid + e * C::TH;
+        const u32 gx = gb + x;
+        const u32 xs = gp ? galois_perm(gx, gp, LOGN) : gx;
+        const u32 xd = gd ? galois_perm(gx, gd, LOGN) : gx;
+        u64 h = 0, lo = 0;
+#pragma unroll 4
+        for (int j = 0; j < l; j++) mac128(h, lo, j == i ? db[xd] : eb[j * estride + xs], __ldg(key + j * kstride + gx));
+        if (ad) mac128(h, lo, ad[ga ? galois_perm(gx, ga, LOGN) : gx], pr);
+        if (ac) mac128(h, lo, ac[gx], pr);
+        const u64 base = mont_reduce(h, lo, M.q, M.qinv);
+        const u64 t = sm[C::pad(x)];
+        out[x] = lazy ? shoup(base + Bq - t, f, fsh, M.q) : shoup(subm(base, red_any(t, M.q, M.mu, M.nq), M.q), f, fsh, M.q);
+    }
+}
+
 // out = a + b over [count][2][l][n]
 __global__ void k_add(const u64 *__restrict__ a, const u64 *__restrict__ b, u64 *__restrict__ out, long long total,
                       int l, int logn, const ModInfo *__restrict__ mods) {
