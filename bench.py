@@ -358,7 +358,9 @@ def run_rotation(args, rank, world, local_rank):
             "peak_source": "measured live: k_peak_modmul (chained 64-bit Shoup modmuls, all SMs; the faster of "
                            "the exact- and approximate-quotient forms)",
             "peaks_gmodmul": {k: v / 1e9 for k, v in peaks.items()},
-            "hbm_gbs": d["gbs"], "hbm_peak_gbs": _hbm_peak(), "traffic": _ncu_traffic(dominant),
+            "hbm_gbs": d["gbs"], "hbm_peak_gbs": _hbm_peak(),
+            "traffic": (_ncu_traffic(dominant) or {}).get("bytes_per_launch"),
+            "traffic_source": (_ncu_traffic(dominant) or {}).get("source"),
             "algorithmic": "per ciphertext: l*l NTTs of (n/2)log2(n) modmuls (k_modup); see DESIGN.md section 3",
         }
     return result
