@@ -913,11 +913,11 @@ def main():
     res = run_rotation(args, rank, world, local_rank)
     if not args.no_inference:
         # secondary line item: configs[2]-shaped inference on a bounded sample per GPU
-        inf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=1, warmup=1,
+        inf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=2, warmup=1,
                             schedule="reference")
         res["inference"] = inf
         res["rates"]["images_per_s"] = inf["images_per_s"]
-        hinf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=1, warmup=1,
+        hinf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=2, warmup=1,
                              schedule="hoisted")
         res["inference_hoisted"] = {k: hinf[k] for k in ("schedule", "images_per_s", "e2e_images_per_s",
                                                          "logical_rotations_per_chunk", "roofline",
