@@ -284,7 +284,7 @@ def run_rotation(args, rank, world, local_rank):
     host_in = torch.from_numpy(slots.view(np.int64)).pin_memory()
     host_out = torch.empty_like(host_in).pin_memory()
     in_np, out_np = host_in.numpy().view(np.uint64), host_out.numpy().view(np.uint64)
-    e2e_chunks = 8
+    e2e_chunks = _env_int("BENCH_E2E_CHUNKS", 8)
     bounds = [(B * i // e2e_chunks, B * (i + 1) // e2e_chunks) for i in range(e2e_chunks)]
 
     def e2e_step():
