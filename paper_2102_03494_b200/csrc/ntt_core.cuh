@@ -39,9 +39,12 @@ struct FwdLazy {
     // inputs < 4q; call once per stage, before its butterflies
     DEV void stage() {
         red = B + 3 > lim;
-        B = red ? max(lim >> 1, B - (lim >> 1)) + 3 : B + 3;
+        B = red ? max((lim >> 1) + 1, B - (lim >> 1)) + 3 : B + 3;
     }
-    DEV u64 cred(u64 u) const { return u >= cq ? u - cq : u; }
+    // approximate conditional subtraction on the high words: u >= cq is certain when
+    // hi(u) > hi(cq); otherwise u < cq + 2^32 < cq + q (reductions only happen for
+    // q >= 2^58, where LIM q would otherwise overflow), hence the "+ 1" in stage()
+    DEV u64 cred(u64 u) const { return (u32)(u >> 32) > (u32)(cq >> 32) ? u - cq : u; }
     DEV void bfly(u64 &a, u64 &b, const ulonglong2 &tw) const {
         const u64 U = a, V = shoup_approx(b, tw.x, tw.y, nq);
         a = U + V;
