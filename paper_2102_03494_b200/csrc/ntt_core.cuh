@@ -258,17 +258,23 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
 #ifndef NTT_LOGL
 #define NTT_LOGL 14      // rows up to 2^NTT_LOGL words run on one CTA
 #endif
+#ifndef NTT_LOGL_BIG
+#define NTT_LOGL_BIG 14  // words per CTA of the cluster rows (n = 2^15, 2^16)
+#endif
 // WO != 0 overrides the radix of single-CTA rows (k_modup and k_ntt_rows run radix-32
 // forward passes: they are faster there, k_rescale is not -- DESIGN.md section 5)
 template <int LOGN, bool INV, int WO = 0>
 struct RowCfg {
-    static constexpr int LOGL = LOGN > 14 ? 14 : (LOGN > NTT_LOGL ? NTT_LOGL : LOGN);    // log2 words per CTA
+    static constexpr int LOGL = LOGN > 14 ? NTT_LOGL_BIG : (LOGN > NTT_LOGL ? NTT_LOGL : LOGN);    // log2 words per CTA
     static constexpr int CL = LOGN - LOGL;                // log2 CTAs per row
     static constexpr int CR = 1 << CL;
-    using Loc = NttCfg<LOGL, (WO && CL == 0) ? WO : (INV ? DefaultWInv<LOGL>::value : DefaultW<LOGL>::value)>;
+#ifndef NTT_WO_CLUSTER
+#define NTT_WO_CLUSTER 0   // 1: the radix override applies to cluster rows too
+#endif
+    using Loc = NttCfg<LOGL, (WO && (CL == 0 || NTT_WO_CLUSTER)) ? WO : (INV ? DefaultWInv<LOGL>::value : DefaultW<LOGL>::value)>;
     static constexpr int W = Loc::W, E = Loc::E, TH = Loc::TH, NL = Loc::N, N = 1 << LOGN;
     static constexpr int SMEM_WORDS = Loc::SMEM_WORDS;
-    static_assert(CL <= 2 && CL <= W, "rows up to 2^16 words");
+    static_assert(CL <= 3 && CL <= W, "clusters of at most 8 CTAs");
     static DEV int pad(int i) { return Loc::pad(i); }
     static DEV int rank() {
         if constexpr (CL > 0) return (int)(blockIdx.x & (CR - 1));
@@ -280,10 +286,10 @@ struct RowCfg {
     static DEV int io(int tid, int e) { return (e << (LOGN - W)) | (rank() * TH + tid); }
 };
 
-template <int LOGN, bool CANON = true>
-DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false>::E], u64 *sm, const ModInfo &M, int tid) {
+template <int LOGN, bool CANON = true, int WO = 0>
+DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false, WO>::E], u64 *sm, const ModInfo &M, int tid) {
     namespace cg = cooperative_groups;
-    using R = RowCfg<LOGN, false>;
+    using R = RowCfg<LOGN, false, WO>;
     constexpr int W = R::W, E = R::E, LOGL = R::LOGL, CL = R::CL;
     FwdLazy Lz(M);
     const int rank = R::rank(), gtid = rank * R::TH + tid;
@@ -439,7 +445,7 @@ template <int LOGN, bool CANON = true, int WO = 0>
 DEV int ntt_fwd_row(u64 (&v)[RowCfg<LOGN, false, WO>::E], u64 *sm, const ModInfo &M, int tid) {
     if constexpr (RowCfg<LOGN, false, WO>::CL == 0)
         return ntt_fwd_core<LOGN, RowCfg<LOGN, false, WO>::W, CANON>(v, sm, M, tid);
-    else return ntt_fwd_cluster<LOGN, CANON>(v, sm, M, tid);
+    else return ntt_fwd_cluster<LOGN, CANON, WO>(v, sm, M, tid);
 }
 #ifndef NTT_W_FUSED_FWD
 #define NTT_W_FUSED_FWD 5
