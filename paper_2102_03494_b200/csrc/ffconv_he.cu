@@ -1094,7 +1094,6 @@ extern "C" int fhe_encrypt(fhe_ctx *c, const uint64_t *slots, uint32_t nonce, fh
     }
     TRY(slots_to_coef(c, s_dev, m, (int)cnt, ct->R));
     if (async) CU(cudaEventRecord(c->ev_in_free[j], c->st));
-    long long total = (long long)cnt * L * n;
     const long long total8 = (long long)cnt * ((n + 7) / 8);
     EW(k_enc_prep, total8, m, tmp, total8, (int)L, (int)ct->R, (int)c->logn, c->P.seed, nonce, c->d_lv + L, c->t_id0,
        c->d_mods);

@@ -53,7 +53,7 @@ struct ModMap {
 //   load 0: plain (< 4q)   1: reduce any 64-bit word   2: centered lift from
 //           source modulus srcmap (values in [0, m_src))
 //   epi  0: store canonical   1: store Montgomery form   2: dst += v
-//        3: encryption, row r = (ci, i): c1 = a (uniform, ChaCha20 as in k_enc_finish),
+//        3: encryption, row r = (ci, i): c1 = a (uniform mod q: ChaCha20 domain ENC_A, 128 bits per coefficient),
 //           c0 = v - a s, with c0 at dst and c1 at dst + c1off
 struct NttRowsArgs {
     const u64 *src;
@@ -646,52 +646,6 @@ __global__ void k_enc_prep(const u64 *__restrict__ m, u64 *__restrict__ tmp, lon
                 if (x0 + u < n) dst[u] = addm(e[u] >= 0 ? (u64)e[u] : M.q - (u64)(-e[u]),     // |e| <= 21 < q
                                              scaled_msg_i(*T, k, mv[u], corr[u], i, M), M.q);
         }
-    }
-}
-
-// encryption, after the NTT: c1 = a (uniform, NTT domain), c0 = tmp - a*s.
-// One thread per 4 coefficients of one (ciphertext, limb): one ChaCha20 block
-// gives their four 128-bit uniform draws.
-__global__ void k_enc_finish(const u64 *__restrict__ tmp, u64 *__restrict__ ct, const u64 *__restrict__ s_m,
-                             long long total4, int L, int logn, u64 seed, u32 nonce, const ModInfo *__restrict__ mods) {
-    const long long n = 1ll << logn;
-    GRID_STRIDE(idx, total4) {
-        const int lper = logn > 2 ? logn - 2 : 0;           // log2 of the 4-coefficient groups per row
-        const u32 row = (u32)(idx >> lper);                 // ci * L + i
-        const int i = (int)(row % (u32)L);
-        const u32 ci = row / (u32)L;
-        const u32 x0 = (u32)(idx & ((1ll << lper) - 1)) * 4;
-        const ModInfo &M = mods[i];
-        u32 blk[16];
-        chacha_block(blk, seed, x0 >> 2, DOM_ENC_A, i, nonce, ci);
-        u64 *c = ct + ((long long)ci * 2 * L) * n;
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const u32 x = x0 + u;
-            if (x >= n) break;
-            const u128 v = ((u128)blk[4 * u + 3] << 96) | ((u128)blk[4 * u + 2] << 64) | ((u128)blk[4 * u + 1] << 32) |
-                           blk[4 * u];
-            const u64 a = mod128(v, M);
-            const u64 as = mont(a, s_m[(long long)i * n + x], M.q, M.qinv);
-            c[((long long)0 * L + i) * n + x] = subm(tmp[(long long)row * n + x], as, M.q);
-            c[((long long)1 * L + i) * n + x] = a;
-        }
-    }
-}
-
-// decryption: x = c0 + c1 * s over [count][l][n]
-__global__ void k_dec_mul(const u64 *__restrict__ ct, const u64 *__restrict__ s_m, u64 *__restrict__ out,
-                          long long total, int l, int logn, const ModInfo *__restrict__ mods) {
-    const long long n = 1ll << logn;
-    GRID_STRIDE(idx, total) {
-        const u32 row = (u32)(idx >> logn);
-        const int i = (int)(row % (u32)l);
-        const long long ci = row / (u32)l;
-        const long long x = idx & (n - 1);
-        const ModInfo &M = mods[i];
-        const u64 *c = ct + ci * 2 * l * n;
-        const u64 c0 = c[(long long)i * n + x], c1 = c[((long long)l + i) * n + x];
-        out[idx] = addm(c0, mont(c1, s_m[(long long)i * n + x], M.q, M.qinv), M.q);
     }
 }
 
