@@ -1257,7 +1257,26 @@ struct KsOut {
 };
 
 // ModUp: every off-diagonal (digit, prime) pair of S cts into Ext
+template <int LOGN>
+static void launch_modup_persist(fhe_ctx *c, int S, u32 l, const DigitTab &dt) {
+    static int sms = 0;
+    if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
+    const int rows = S * (int)(l * l);
+    launch_row<LOGN, false, FwdW5<LOGN>::value>(c, "k_modup", k_modup_persist<LOGN>, dim3(std::min(rows, sms)), c->st,
+                                                 dt, c->w_Ext, (int)l, c->special_id, rows, c->d_mods);
+    c->alg_mm += (double)(rows - std::min(rows, sms)) * (c->n / 2) * c->logn;   // launch_row counted one row per CTA
+}
+
 static int keyswitch_modup(fhe_ctx *c, int S, u32 l, const DigitTab &dt) {
+    static int persist = -1;     // FHE_MODUP_PERSIST: persistent ModUp CTAs (single-CTA rows)
+    if (persist < 0) { const char *e = getenv("FHE_MODUP_PERSIST"); persist = e ? atoi(e) : 1; }
+    if (persist && c->logn <= 14 && c->logn >= 12) {
+        if (c->logn == 14) launch_modup_persist<14>(c, S, l, dt);
+        else if (c->logn == 13) launch_modup_persist<13>(c, S, l, dt);
+        else launch_modup_persist<12>(c, S, l, dt);
+        CHECK_LAUNCH();
+        return 0;
+    }
     c->alg_mm -= (double)S * l * (c->n / 2) * c->logn;      // the diagonal rows return at once
     LOGN_SWITCH(c->logn, launch_row<LG, false, FwdW5<LG>::value>(c, "k_modup", k_modup<LG>, dim3(S, l, l + 1), c->st, dt, c->w_Ext, (int)l, c->special_id,
                                         c->d_mods));

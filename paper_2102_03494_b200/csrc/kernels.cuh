@@ -235,12 +235,9 @@ struct DigitTab {
 // into prime i (i == l: the special prime) and transformed; the diagonal i == j is
 // skipped (the inner product reads it from DigitTab.ntt).
 template <int LOGN>
-__global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
-                                                             const ModInfo *__restrict__ mods) {
+DEV void modup_row(const DigitTab &dt, u64 *Ext, int l, int special_id, const ModInfo *__restrict__ mods, int s, int j,
+                   int i, u64 *sm, int tid) {
     using C = RowCfg<LOGN, false, FwdW5<LOGN>::value>;
-    extern __shared__ u64 sm[];
-    const int s = C::row(), j = blockIdx.y, i = blockIdx.z, tid = threadIdx.x;
-    if (i == j) return;
     const long long n = C::N;
     const ModInfo M = mods[i == l ? special_id : i];
     const ModInfo &Sj = mods[j];
@@ -258,6 +255,39 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k
         for (int x = tid; x < C::NL; x += C::TH) dst[x] = sm[C::pad(x)];
     } else {
         for (int x = tid; x < C::NL; x += C::TH) dst[x] = red_any(sm[C::pad(x)], M.q, M.mu, M.nq);
+    }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k_modup(DigitTab dt, u64 *Ext, int l, int special_id,
+                                                             const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false, FwdW5<LOGN>::value>;
+    extern __shared__ u64 sm[];
+    const int s = C::row(), j = blockIdx.y, i = blockIdx.z;
+    if (i == j) return;
+    modup_row<LOGN>(dt, Ext, l, special_id, mods, s, j, i, sm, threadIdx.x);
+}
+
+// Persistent ModUp (single-CTA rows): CTA b walks the off-diagonal rows b, b + grid, ...
+// and prefetches the next row's digit into L2 while transforming the current one.
+template <int LOGN>
+__global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k_modup_persist(DigitTab dt, u64 *Ext, int l,
+                                                                     int special_id, int rows,
+                                                                     const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false, FwdW5<LOGN>::value>;
+    static_assert(C::CL == 0, "persistent ModUp: single-CTA rows only");
+    extern __shared__ u64 sm[];
+    const int tid = threadIdx.x, ll = l * l;
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int s = r / ll, rem = r % ll, j = rem / l, ii = rem % l, i = ii < j ? ii : ii + 1;
+        const int rn = r + gridDim.x;
+        if (tid == 0 && rn < rows) {
+            const int sn = rn / ll, jn = (rn % ll) / l;
+            const u64 *nsrc = dt.coef[sn] + (long long)jn * C::N;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nsrc), "r"((u32)(C::N * 8)) : "memory");
+        }
+        modup_row<LOGN>(dt, Ext, l, special_id, mods, s, j, i, sm, tid);
+        __syncthreads();          // the next row's NTT reuses the shared memory
     }
 }
 
