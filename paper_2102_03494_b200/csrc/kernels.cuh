@@ -317,10 +317,9 @@ struct RescaleW {
     static constexpr int value = LOGN >= 12 ? NTT_W_RESCALE : 0;
 };
 template <int LOGN>
-__global__ void __launch_bounds__(RowCfg<LOGN, false, RescaleW<LOGN>::value>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
+DEV void rescale_row(const RescaleArgs &a, const ModInfo *__restrict__ mods, int s, int p, int i, u64 *sm, int tid) {
     using C = RowCfg<LOGN, false, RescaleW<LOGN>::value>;
-    extern __shared__ u64 sm[];
-    const int s = C::row(), p = blockIdx.y, i = blockIdx.z, tid = threadIdx.x, gb = C::base();
+    const int gb = C::base();
     const long long n = C::N;
     const ModInfo M = mods[i];
     const ModInfo &S = mods[a.src_id];
@@ -381,6 +380,14 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false, RescaleW<LOGN>::value>::TH
 #pragma unroll
     for (int e = 0; e < C::E; e++) out[tid + e * C::TH] = y[e];
 }
+
+template <int LOGN>
+__global__ void __launch_bounds__(RowCfg<LOGN, false, RescaleW<LOGN>::value>::TH) k_rescale(RescaleArgs a, const ModInfo *__restrict__ mods) {
+    using C = RowCfg<LOGN, false, RescaleW<LOGN>::value>;
+    extern __shared__ u64 sm[];
+    rescale_row<LOGN>(a, mods, C::row(), blockIdx.y, blockIdx.z, sm, threadIdx.x);
+}
+
 
 // ========================================================= elementwise kernels
 
