@@ -47,3 +47,16 @@ def test_boundary_errors(golden_lib):
         ev.mod_switch(low)
     with pytest.raises(FheError):
         ev.add(ct, low)
+
+
+def test_empty_batches_golden(golden_lib):
+    """Zero-length batch calls are no-ops that return empty lists (the same calls run
+    against the CUDA library in test_gpu_parity.py::test_empty_batches)."""
+    P = make_params(16, [65537], levels=3, q_bits=50)
+    ev = Evaluator(P, golden_lib)
+    ct = ev.encrypt(np.zeros((1, 1, 32), dtype=np.uint64))
+    assert ev.rotate_many([], 3) == []
+    assert ev.rotate_multi([], []) == []
+    assert ev.rotate_hoisted(ct, []) == []
+    assert ev.mul_plain_many([], []) == []
+    assert ev.add_many([], []) == []

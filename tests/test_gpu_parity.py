@@ -29,6 +29,8 @@ CASES = [
     (1024, [65537], 3, 58),
     (8192, [65537], 3, 60),
     (64, [65537], 7, 61),
+    # many levels: key-switch paths at l = 12 (templated inner product, runtime-l special rows)
+    (64, [65537], 12, 40),
     # rings 2^15 / 2^16: one row per thread-block cluster of 2 / 4 CTAs (DSMEM NTT)
     (16384, [65537], 3, 50),
     (32768, [786433], 3, 50),
@@ -253,3 +255,15 @@ def test_rotate_hoisted_bit_exact(case, golden_lib, cuda_lib, monkeypatch):
     outs = gp.rotate_hoisted(cc, ks)
     for k, o in zip(ks, outs):
         assert np.array_equal(gd.read(gd.rotate(cg, k)), gp.read(o)), k
+
+
+def test_empty_batches(golden_lib, cuda_lib):
+    """Zero-length batch calls launch nothing and return empty lists (both libraries)."""
+    gd, gp, P = _pair(CASES[1], golden_lib, cuda_lib)
+    for ev in (gd, gp):
+        ct = ev.encrypt(_rand_slots(P, 1, np.random.default_rng(9)))
+        assert ev.rotate_many([], 3) == []
+        assert ev.rotate_multi([], []) == []
+        assert ev.rotate_hoisted(ct, []) == []
+        assert ev.mul_plain_many([], []) == []
+        assert ev.add_many([], []) == []
