@@ -628,8 +628,10 @@ DEV u64 scaled_corr(const LevelDev &T, int k, u64 t, u64 m) {
     while (rem >= t) { rem -= t; est++; }
     return est + (2 * (u64)rem >= t ? 1 : 0);
 }
+// m < t < 2^61 and delta < q, so m * delta < q 2^64: the Montgomery product needs no
+// prior reduction of m
 DEV u64 scaled_msg_i(const LevelDev &T, int k, u64 m, u64 corr, int i, const ModInfo &Mq) {
-    return addm(mont(red64(m, Mq.q, Mq.mu), T.delta_m[k][i], Mq.q, Mq.qinv), red64(corr, Mq.q, Mq.mu), Mq.q);
+    return addm(mont(m, T.delta_m[k][i], Mq.q, Mq.qinv), red_any(corr, Mq.q, Mq.mu, Mq.nq), Mq.q);
 }
 DEV u64 scaled_msg(const LevelDev &T, int k, u64 t, u64 m, int i, const ModInfo &Mq) {
     return scaled_msg_i(T, k, m, scaled_corr(T, k, t, m), i, Mq);
