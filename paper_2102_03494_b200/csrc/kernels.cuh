@@ -505,7 +505,11 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_ks_special(const u64
     const u32 es = dt.perm[s] ? dt.esrc[s] : (u32)s;
     const u64 *eb = Ext + (es * l * (l + 1) + l) * n;
     const u32 g = dt.perm[s];
-#pragma unroll
+#ifndef KSP_UNROLL
+#define KSP_UNROLL 2         // element loop of the special-row inner product (measured: 2 > 4 > 16)
+#endif
+    constexpr int kKspUnroll = KSP_UNROLL;
+#pragma unroll (kKspUnroll)
     for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) {
         const u32 gx = base + x;
         const u32 xs = g ? galois_perm(gx, g, LOGN) : gx;
