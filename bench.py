@@ -288,10 +288,10 @@ def run_rotation(args, rank, world, local_rank):
     bounds = [(B * i // e2e_chunks, B * (i + 1) // e2e_chunks) for i in range(e2e_chunks)]
 
     def e2e_step():
-        cs = [ev.encrypt(in_np[:, r0:r1]) for r0, r1 in bounds]
+        cs = [ev.encrypt(in_np[:, r0:r1], async_=True) for r0, r1 in bounds]
         rs = ev.rotate_many(cs, k)                     # one key-switching launch sequence
         for (r0, r1), r in zip(bounds, rs):
-            ev.decrypt(r, out=out_np[:, r0:r1])
+            ev.decrypt(r, out=out_np[:, r0:r1], async_=True)
 
     e2e_steps = max(1, min(args.steps, 5))
     for _ in range(1):
@@ -383,7 +383,7 @@ def cfg0_setup(images: int, seed: int, offset: int = 0):
     shape = TensorShape(29, 29, 1)
     prov = NetworkSpec(SchemeParams(n_slots=8192, t=(1 << 61) - 1), shape, layers)
     ws = synthetic_weights(prov, np.random.default_rng(seed), sigma=0.1)
-    rp = inference_params(prov, build_plan(prov, "explicit"), ws, input_bound=255)
+    rp = inference_params(prov, build_plan(prov, "explicit"), ws, input_bound=255, seed=CFG1["seed"])
     net = NetworkSpec(scheme_for(rp), shape, layers)
     plan = build_plan(net, "explicit")
     rng = np.random.default_rng(seed + 1)
@@ -426,7 +426,7 @@ def cfg3_setup(images: int, seed: int, offset: int = 0):
     for name, scale in meta["scales"].items():
         ws.add(WeightTensor(name, z[name.replace(".", "_")].astype(np.int64), 8, scale))
     prov = NetworkSpec(SchemeParams(n_slots=meta["n_slots"], t=(1 << 61) - 1), shape, layers)
-    rp = inference_params(prov, build_plan(prov, meta["strategy"]), ws, input_bound=255)
+    rp = inference_params(prov, build_plan(prov, meta["strategy"]), ws, input_bound=255, seed=CFG1["seed"])
     net = NetworkSpec(scheme_for(rp), shape, layers)
     plan = build_plan(net, meta["strategy"])
     fx = z["inputs"].astype(np.int64)
@@ -533,7 +533,7 @@ def ablation_setup(first, images, seed, offset=0):
     shape = TensorShape(29, 29, 1)
     prov = NetworkSpec(SchemeParams(n_slots=8192, t=(1 << 61) - 1), shape, layers)
     ws = synthetic_weights(prov, np.random.default_rng(seed), sigma=0.1)
-    rp = inference_params(prov, build_plan(prov, "explicit"), ws, input_bound=255)
+    rp = inference_params(prov, build_plan(prov, "explicit"), ws, input_bound=255, seed=CFG1["seed"])
     net = NetworkSpec(scheme_for(rp), shape, layers)
     rng = np.random.default_rng(seed + 1)
     pix = np.round(rng.random(size=(offset + images, 1, 28, 28)) * 255).astype(np.int64)[offset:]

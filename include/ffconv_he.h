@@ -138,6 +138,18 @@ int fhe_pt_read(fhe_ctx *ctx, const fhe_pt *pt, uint64_t *words);
  * valid only after fhe_sync().  Pageable buffers are copied synchronously. */
 int fhe_encrypt(fhe_ctx *ctx, const uint64_t *slots, uint32_t nonce, fhe_ct *out);
 int fhe_decrypt(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *slots);
+/* Deferred checks (no host synchronization on the evaluation path):
+ * fhe_check_zero_tail enqueues the rotate_and_sum precondition of the reference
+ * (hesim.py:360-361: every slot at index >= m is zero) for every physical
+ * ciphertext of ct and both batching rows; a violation sets bit 0 of the sticky
+ * flags.  Every decryption (fhe_decrypt, fhe_check_zero_tail) max-reduces the
+ * distance of t x / Q to the nearest integer over all coefficients (the invariant
+ * noise, top 32 bits of the fraction, units of 2^-32): a value near 2^31 means
+ * the noise budget is exhausted and the decrypted slots are garbage.
+ * fhe_status synchronizes the context's stream and reads (and with reset != 0
+ * clears) both. */
+int fhe_check_zero_tail(fhe_ctx *ctx, const fhe_ct *ct, uint32_t m);
+int fhe_status(fhe_ctx *ctx, uint32_t *noise_dist, uint32_t *flags, int reset);
 /* diagnostic: coefficient-form x = c0 + c1*s over Q_level, [T*R][level][n]
  * (the caller derives the exact invariant noise |[t x]_Q| / Q from it) */
 int fhe_decrypt_raw(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *coef);

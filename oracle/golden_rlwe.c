@@ -320,6 +320,8 @@ struct fhe_ctx {
     aux_tab ax;
     key_node *keys;
     u64 key_bytes;
+    uint32_t noise_max;  /* largest decryption rounding distance since the last fhe_status (2^-32 units) */
+    uint32_t flags;      /* bit 0: rotate_and_sum precondition violated (fhe_check_zero_tail) */
 };
 
 struct fhe_ct {
@@ -714,7 +716,7 @@ static void raw_one(const fhe_ctx *c, const fhe_ct *ct, u32 ci, u64 *x) {
 }
 
 /* m = round(t x / Q_l) mod t via the 128-bit fixed-point sum of y_i t / q_i */
-static void decrypt_one(const fhe_ctx *c, const fhe_ct *ct, u32 ci, u64 *coef) {
+static void decrypt_one(fhe_ctx *c, const fhe_ct *ct, u32 ci, u64 *coef) {
     u32 n = c->n, l = ct->level, k = ci / ct->R;
     u64 t = c->P.t[k];
     const level_tab *T = &c->lv[l];
@@ -727,6 +729,8 @@ static void decrypt_one(const fhe_ctx *c, const fhe_ct *ct, u32 ci, u64 *coef) {
             fx_acc(&ai, &af, y, T->decW[k][i], T->decF[k][i]);
         }
         coef[j] = (u64)((ai + (af >> 127)) % t);
+        uint32_t f = (uint32_t)(af >> 96), d = (f >> 31) ? 0u - f : f;
+        if (d > c->noise_max) c->noise_max = d;
     }
     free(x);
 }
@@ -738,6 +742,27 @@ int fhe_decrypt(fhe_ctx *c, const fhe_ct *ct, uint64_t *slots) {
         coef_to_slots(c, ci / ct->R, coef, slots + (size_t)ci * c->n);
     }
     free(coef);
+    return 0;
+}
+
+int fhe_check_zero_tail(fhe_ctx *c, const fhe_ct *ct, uint32_t m) {
+    if (m > c->N) return fail(FHE_EINVAL, "check_zero_tail: m = %u exceeds %u slots", m, c->N);
+    if (m == c->N) return 0;
+    u64 *coef = (u64 *)malloc(c->n * 8), *slots = (u64 *)malloc(c->n * 8);
+    for (u32 ci = 0; ci < ct->count; ci++) {
+        decrypt_one(c, ct, ci, coef);
+        coef_to_slots(c, ci / ct->R, coef, slots);
+        for (u32 x = 0; x < c->n; x++)
+            if ((x % c->N) >= m && slots[x]) c->flags |= 1u;
+    }
+    free(coef); free(slots);
+    return 0;
+}
+
+int fhe_status(fhe_ctx *c, uint32_t *noise_dist, uint32_t *flags, int reset) {
+    if (noise_dist) *noise_dist = c->noise_max;
+    if (flags) *flags = c->flags;
+    if (reset) { c->noise_max = 0; c->flags = 0; }
     return 0;
 }
 

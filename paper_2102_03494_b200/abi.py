@@ -78,6 +78,8 @@ SIGNATURES = {
     "fhe_encrypt": (c_int, [c_void_p, _U64P, c_uint32, c_void_p]),
     "fhe_decrypt": (c_int, [c_void_p, c_void_p, _U64P]),
     "fhe_decrypt_raw": (c_int, [c_void_p, c_void_p, _U64P]),
+    "fhe_check_zero_tail": (c_int, [c_void_p, c_void_p, c_uint32]),
+    "fhe_status": (c_int, [c_void_p, POINTER(c_uint32), POINTER(c_uint32), c_int]),
     "fhe_add": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fhe_mul_plain": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fhe_mul_plain_acc": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

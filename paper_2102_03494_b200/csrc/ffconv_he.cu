@@ -136,6 +136,8 @@ struct fhe_ctx {
     AuxDev hax{};
     AuxDev *d_ax = nullptr;
     u64 *d_pmod = nullptr;             // P mod prime_i, i in [0, L]
+    u32 *d_status = nullptr;           // [0] largest decryption rounding distance (2^-32 units)
+                                       // [1] sticky flags: bit 0 rotate_and_sum precondition violated
     u64 pinv[MAXQ]{}, pinv_sh[MAXQ]{};
     u64 pmont[MAXQ]{};                  // P * 2^64 mod q_i (key-switch addends, KsAdd)
     std::unordered_map<u32, KeyBuf> keys;
@@ -535,6 +537,8 @@ static int setup_secret(fhe_ctx *c) {
     }
     CU(cudaMalloc((void **)&c->d_pmod, (c->L + 1) * 8));
     CU(cudaMemcpy(c->d_pmod, pm.data(), (c->L + 1) * 8, cudaMemcpyHostToDevice));
+    CU(cudaMalloc((void **)&c->d_status, 2 * sizeof(u32)));
+    CU(cudaMemset(c->d_status, 0, 2 * sizeof(u32)));
     return 0;
 }
 
@@ -662,7 +666,7 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
         for (cudaEvent_t e : evs) if (e) cudaEventDestroy(e);
     }
     void *bufs[] = {c->d_mods, c->d_tw, c->d_s_can, c->d_s_m, c->d_s2_m, c->d_sk_ids, c->d_slot2ntt,
-                    c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_sq};
+                    c->d_ntt2slot, c->d_lv, c->d_ax, c->d_pmod, c->w_sq, c->d_status};
     for (void *b : bufs) if (b) cudaFree(b);
     for (int k = 0; k < fhe_ctx::MAXLANES; k++) {
         void *wb[] = {c->ws_D[k], c->ws_Ext[k], c->ws_Acc[k]};
@@ -1131,19 +1135,27 @@ static int raw_decrypt(fhe_ctx *c, const fhe_ct *ct, u64 *dst) {
     return intt_rows(c, (int)(ct->count * l), a);
 }
 
-extern "C" int fhe_decrypt(fhe_ctx *c, const fhe_ct *ct, uint64_t *slots) {
+// decrypted slot values mod t_k in NTT order, [cnt][n], into m (scratch X: [cnt][l][n])
+static int decode_ntt_order(fhe_ctx *c, const fhe_ct *ct, u64 *X, u64 *m) {
     size_t n = c->n, l = ct->level, cnt = ct->count;
-    TRY(ensure_tmp(c, cnt * n * (l + 2)));
-    u64 *X = c->w_tmp, *m = X + cnt * l * n, *o = m + cnt * n;
     TRY(raw_decrypt(c, ct, X));
     long long total = (long long)cnt * n;
-    EW(k_dec_scale, total, X, m, total, (int)l, (int)ct->R, (int)c->logn, c->d_lv + l, c->t_id0, c->d_mods);
+    EW(k_dec_scale, total, X, m, total, (int)l, (int)ct->R, (int)c->logn, c->d_lv + l, c->t_id0, c->d_mods,
+       c->d_status);
     CHECK_LAUNCH();
     NttRowsArgs a = nargs(m, m, n);
     a.div = ct->R;
     a.period = c->T;
     map_range(a.map, c->T, c->t_id0);
-    TRY(ntt_rows(c, (int)cnt, a));
+    return ntt_rows(c, (int)cnt, a);
+}
+
+extern "C" int fhe_decrypt(fhe_ctx *c, const fhe_ct *ct, uint64_t *slots) {
+    size_t n = c->n, l = ct->level, cnt = ct->count;
+    TRY(ensure_tmp(c, cnt * n * (l + 2)));
+    u64 *X = c->w_tmp, *m = X + cnt * l * n, *o = m + cnt * n;
+    TRY(decode_ntt_order(c, ct, X, m));
+    long long total = (long long)cnt * n;
     if (is_pinned(slots)) {
         // pinned output: gather into staging slot j, D2H on the copy stream; valid after fhe_sync
         const int j = c->io_out_next;
@@ -1162,6 +1174,29 @@ extern "C" int fhe_decrypt(fhe_ctx *c, const fhe_ct *ct, uint64_t *slots) {
     CHECK_LAUNCH();
     CU(cudaMemcpyAsync(slots, o, cnt * n * 8, cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
+extern "C" int fhe_check_zero_tail(fhe_ctx *c, const fhe_ct *ct, uint32_t m) {
+    if (m > c->N) return fail(FHE_EINVAL, "check_zero_tail: m = %u exceeds %u slots", m, c->N);
+    if (m == c->N) return 0;
+    size_t n = c->n, l = ct->level, cnt = ct->count;
+    TRY(ensure_tmp(c, cnt * n * (l + 1)));
+    u64 *X = c->w_tmp, *mc = X + cnt * l * n;
+    TRY(decode_ntt_order(c, ct, X, mc));
+    long long total = (long long)cnt * n;
+    EW(k_tail_check, total, mc, total, (int)c->logn, m, c->d_ntt2slot, c->d_status + 1);
+    CHECK_LAUNCH();
+    return 0;
+}
+
+extern "C" int fhe_status(fhe_ctx *c, uint32_t *noise_dist, uint32_t *flags, int reset) {
+    u32 h[2];
+    CU(cudaStreamSynchronize(c->st));
+    CU(cudaMemcpy(h, c->d_status, sizeof h, cudaMemcpyDeviceToHost));
+    if (reset) CU(cudaMemset(c->d_status, 0, sizeof h));
+    if (noise_dist) *noise_dist = h[0];
+    if (flags) *flags = h[1];
     return 0;
 }
 

@@ -696,10 +696,16 @@ __global__ void k_enc_prep(const u64 *__restrict__ m, u64 *__restrict__ tmp, lon
     }
 }
 
-// decryption: per coefficient m = round(t x / Q_l) mod t via the fixed-point sum
+// decryption: per coefficient m = round(t x / Q_l) mod t via the fixed-point sum.
+// Noise guard: the fractional part of t x / Q_l is the invariant noise; its largest
+// distance to an integer (top 32 bits, units of 2^-32) is max-reduced into *noise.
+// A healthy ciphertext leaves it near 2^(32 - budget bits); once the budget is gone
+// the fractions are uniform and the maximum approaches 2^31 (= 1/2).
 __global__ void k_dec_scale(const u64 *__restrict__ X, u64 *__restrict__ m, long long total, int l, int R, int logn,
-                            const LevelDev *__restrict__ T, int t_id0, const ModInfo *__restrict__ mods) {
+                            const LevelDev *__restrict__ T, int t_id0, const ModInfo *__restrict__ mods,
+                            u32 *__restrict__ noise) {
     const long long n = 1ll << logn;
+    u32 dmax = 0;
     GRID_STRIDE(idx, total) {
         const long long ci = idx >> logn;
         const long long x = idx & (n - 1);
@@ -711,7 +717,26 @@ __global__ void k_dec_scale(const u64 *__restrict__ X, u64 *__restrict__ m, long
             fx_acc(ai, af, y, T->decW[k][i], T->decFhi[k][i], T->decFlo[k][i]);
         }
         m[idx] = mod128(ai + (af >> 127), mods[t_id0 + k]);
+        const u32 f = (u32)(af >> 96);
+        const u32 d = f >> 31 ? 0u - f : f;
+        dmax = d > dmax ? d : dmax;
     }
+    dmax = __reduce_max_sync(0xFFFFFFFFu, dmax);
+    if ((threadIdx.x & 31) == 0 && dmax) atomicMax(noise, dmax);
+}
+
+// rotate_and_sum precondition (hesim.py:360-361): flag |= 1 if any decrypted slot at
+// index >= m of either batching row is nonzero.  mcoef: [cnt][n] slot values mod t_k in
+// NTT order (after the decoding NTT), ntt2slot maps an NTT position to a slot index.
+__global__ void k_tail_check(const u64 *__restrict__ mcoef, long long total, int logn, u32 m,
+                             const u32 *__restrict__ ntt2slot, u32 *__restrict__ flag) {
+    const u32 half = 1u << (logn - 1);
+    bool bad = false;
+    GRID_STRIDE(idx, total) {
+        const u32 slot = ntt2slot[idx & ((1ll << logn) - 1)] & (half - 1);
+        bad |= slot >= m && mcoef[idx] != 0;
+    }
+    if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
 
 // out[ci][x] = A[ci][slot2ntt[x]]

@@ -13,8 +13,12 @@ Differences a caller can observe, all deliberate:
   them (images 2r and 2r+1 share the two batching rows of row-pair r);
 * `encrypt`/`decrypt` accept/return one slot vector per image when batch > 1;
 * `ct.slots` is a decrypting property (test convenience, costs a decrypt);
-* the `rotate_and_sum` zero-tail precondition needs a decrypt, so it is only
-  checked when the context was built with `debug_checks=True`;
+* the `rotate_and_sum` zero-tail precondition is checked on the device for every
+  call (a decrypt of the operand and a scan of slots >= m, no host round trip);
+  a violation raises `PreconditionError` at the next synchronizing call
+  (decrypt, `check()`), or immediately with `debug_checks=True`;
+* every decryption checks the noise budget on the device and raises
+  `NoiseBudgetError` instead of returning garbage slots;
 * t must factor into primes = 1 mod 2N (SIMD batching); a composite t is given
   through `SchemeParams.t_factors` and evaluated by plaintext CRT.
 """
@@ -43,6 +47,11 @@ class EncodingOverflowError(ValueError):
 
 class PreconditionError(ValueError):
     """An operation's slot-content precondition is violated."""
+
+
+class NoiseBudgetError(ValueError):
+    """A decrypted ciphertext had no noise budget left: its slots are not the
+    encrypted values (the q chain is too short for the computation)."""
 
 
 @dataclass(frozen=True)
@@ -228,7 +237,7 @@ class HeContext:
 
     def __init__(self, params: SchemeParams, *, batch: int = 1, lib=None, levels: int | None = None,
                  q_bits: int | None = None, debug_checks: bool = False, pt_cache: bool = True,
-                 schedule: str = "reference", hoist_levels: int = 7):
+                 schedule: str = "reference", hoist_levels: int = 7, precondition_checks: bool = True):
         if batch < 1:
             raise ValueError("batch must be >= 1")
         self.params = params
@@ -237,6 +246,8 @@ class HeContext:
         self.batch = batch
         self.rows = (batch + 1) // 2
         self.debug_checks = debug_checks
+        self.precondition_checks = precondition_checks
+        self.last_noise_budget = None
         self._lib = lib
         self._levels = levels
         self._q_bits = q_bits
@@ -319,10 +330,29 @@ class HeContext:
             self._pt_cache_bytes += size
         return pt
 
+    def check(self) -> None:
+        """Synchronize with the device and raise any deferred check failure:
+        PreconditionError (a rotate_and_sum operand had nonzero slots >= m) or
+        NoiseBudgetError (a decryption since the last check had no budget left)."""
+        if self._ev is None:
+            return
+        budget, flags = self._ev.status(reset=True)
+        self.last_noise_budget = budget
+        # the distance to the nearest integer never exceeds 1/2, so an exhausted budget
+        # reads as ~0 bits (uniform fractions); below 0.5 bits (|noise| > 0.35) the
+        # ciphertext is one operation from garbage and is rejected as well
+        if budget < 0.5:
+            raise NoiseBudgetError(f"noise budget exhausted ({budget:.3f} bits left at decryption): the q chain "
+                                   f"is too short for this computation; size it with runner.inference_params")
+        if flags & 1:
+            raise PreconditionError("rotate_and_sum: slots at index >= m must be zero "
+                                    "(detected on the device at an earlier call)")
+
     def _residues(self, ct: SlotCiphertext):
         """Decrypted residues mod t, (N,) for batch 1 else (batch, N)."""
         ev = self.evaluator
         raw = ev.decrypt(ct.handle)                                      # (T, R, 2N) uint64
+        self.check()
         N = self.params.n_slots
         per = np.empty((raw.shape[0], self.batch, N), dtype=np.uint64)
         per[:, 0::2] = raw[:, : (self.batch + 1) // 2, :N]
@@ -636,12 +666,12 @@ class HeContext:
         if not 1 <= m <= n:
             raise ValueError(f"m must be in [1, {n}], got {m}")
         cts = list(cts)
-        if self.debug_checks and m < n:
-            for ct in cts:
-                if ct.tracked:
-                    res = np.asarray(self._residues(ct))
-                    if np.any(res[..., m:]):
-                        raise PreconditionError(f"slots at index >= {m} must be zero")
+        if (self.debug_checks or self.precondition_checks) and m < n:
+            tracked = [ct for ct in cts if ct.tracked]
+            for ct in tracked:
+                self.evaluator.check_zero_tail(ct.handle, m)
+            if self.debug_checks and tracked:
+                self.check()                       # immediate, like the reference (hesim.py:360-361)
         rounds = (m - 1).bit_length()
         acc = cts
         for h in reversed(range(rounds)):

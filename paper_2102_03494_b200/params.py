@@ -16,6 +16,7 @@ prime for key switching and an auxiliary base for ct x ct products.  The rules
 from __future__ import annotations
 
 import math
+import secrets
 from dataclasses import dataclass, field
 
 from .abi import FHE_MAX_B, FHE_MAX_Q, FHE_MAX_T, FheParams
@@ -75,7 +76,9 @@ class RlweParams:
     p: tuple[int, ...]
     t: tuple[int, ...]
     b: tuple[int, ...] = ()
-    seed: int = 0x5EED_F0C0_2102_3494
+    # every key and all encryption randomness derive from the seed: a fresh random one
+    # per parameter set unless pinned (tests, bench, and ranks that must share keys)
+    seed: int = field(default_factory=lambda: secrets.randbits(64))
 
     def __post_init__(self):
         if len(self.q) > FHE_MAX_Q or len(self.b) > FHE_MAX_B or len(self.t) > FHE_MAX_T:

@@ -124,24 +124,50 @@ class Evaluator:
         self.lib.call("fhe_pt_read", self.ctx, pt.ptr, u64_ptr(out))
         return out.reshape(self.T, self.L, self.n)
 
-    def encrypt(self, slots: np.ndarray, nonce: int | None = None) -> Ciphertext:
+    def encrypt(self, slots: np.ndarray, nonce: int | None = None, async_: bool = False) -> Ciphertext:
+        """Encrypt [T][R][n] residues.  With a page-locked `slots` buffer and
+        async_=True the host->device copy runs on the library's copy stream and
+        the call returns at once: `slots` must stay untouched until sync().
+        Otherwise the call returns only after the input has been read."""
         s = np.ascontiguousarray(slots, dtype=np.uint64)
         if s.ndim != 3 or s.shape[0] != self.T or s.shape[2] != self.n:
             raise ValueError(f"slots must have shape (T={self.T}, R, n={self.n})")
         if nonce is None:
             nonce = self._nonce
+            if nonce > 0xFFFFFFFF:
+                raise RuntimeError("encryption nonces exhausted (2^32 encryptions per context)")
             self._nonce += 1
         ct = self.new_ct(s.shape[1])
         self.lib.call("fhe_encrypt", self.ctx, u64_ptr(s), nonce & 0xFFFFFFFF, ct.ptr)
+        if not async_:
+            self.sync()
         return ct
 
-    def decrypt(self, ct: Ciphertext, out: np.ndarray | None = None) -> np.ndarray:
+    def decrypt(self, ct: Ciphertext, out: np.ndarray | None = None, async_: bool = False) -> np.ndarray:
+        """Decrypted [T][R][n] residues.  With a page-locked `out` and async_=True
+        the device->host copy is only enqueued: `out` is valid after sync()."""
         if out is None:
             out = np.empty((self.T, ct.rows, self.n), dtype=np.uint64)
         elif out.dtype != np.uint64 or out.size != self.T * ct.rows * self.n or not out.flags["C_CONTIGUOUS"]:
             raise ValueError("decrypt: out must be a contiguous uint64 array of T*R*n words")
         self.lib.call("fhe_decrypt", self.ctx, ct.ptr, u64_ptr(out))
+        if not async_:
+            self.sync()
         return out.reshape(self.T, ct.rows, self.n)
+
+    def check_zero_tail(self, ct: Ciphertext, m: int) -> None:
+        """Enqueue the rotate_and_sum precondition check (slots >= m zero); a
+        violation shows up in status()."""
+        self.lib.call("fhe_check_zero_tail", self.ctx, ct.ptr, int(m))
+
+    def status(self, reset: bool = True) -> tuple[float, int]:
+        """(smallest noise budget in bits seen by decryptions since the last
+        reset, sticky check flags); synchronizes the context's stream."""
+        d, f = ctypes.c_uint32(), ctypes.c_uint32()
+        self.lib.call("fhe_status", self.ctx, ctypes.byref(d), ctypes.byref(f), int(reset))
+        # distance d / 2^32 to the nearest integer: budget = -log2(2 d / 2^32)
+        budget = 31.0 - math.log2(d.value) if d.value else 32.0
+        return budget, f.value
 
     def decrypt_raw(self, ct: Ciphertext) -> np.ndarray:
         out = np.empty((self.T * ct.rows, ct.level, self.n), dtype=np.uint64)

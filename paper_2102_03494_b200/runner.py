@@ -170,6 +170,22 @@ def inference_params(net: NetworkSpec, plan: PackingPlan, ws: WeightSet, input_b
     return RlweParams(log_n=n_slots.bit_length(), q=tuple(q), p=tuple(p), t=tuple(ts), b=tuple(b), **kw)
 
 
+def default_context(net: NetworkSpec, plan: PackingPlan, input_tensor=None, *, batch: int | None = None,
+                    q_bits: int = 60, mask_fc: bool = True, lib=None) -> HeContext:
+    """A GPU HeContext for net.scheme whose q chain is sized for this plan (the noise
+    model of `inference_params` at the scheme's own plaintext factors) unless the
+    scheme pins its RlweParams.  t must factor into batching-compatible primes."""
+    x = None if input_tensor is None else np.asarray(input_tensor)
+    if batch is None:
+        shape_rank = 3
+        batch = x.shape[0] if x is not None and x.ndim == shape_rank + 1 else 1
+    if net.scheme.rlwe is not None:
+        return HeContext(net.scheme, batch=batch, lib=lib)
+    t_bits = math.log2(max(net.scheme.factors()))
+    levels = max(2, math.ceil(_noise_bits(plan, t_bits, mask_fc) / q_bits))
+    return HeContext(net.scheme, batch=batch, lib=lib, levels=levels, q_bits=q_bits)
+
+
 def scheme_for(params: RlweParams, rotation_weight: float = 10.0) -> SchemeParams:
     """A SchemeParams whose t is the CRT product of the chosen plaintext primes."""
     return SchemeParams(n_slots=params.n_slots, t=params.t_product, rotation_weight=rotation_weight,
@@ -252,7 +268,7 @@ def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input
     if plan.net != net:
         raise ValueError("plan was built for a different network")
     if ctx is None:
-        ctx = HeContext(net.scheme)
+        ctx = default_context(net, plan, input_tensor)
     x_in = None
     if track_values and packed is None:
         x_in = np.asarray(input_tensor)

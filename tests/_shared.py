@@ -21,8 +21,8 @@ def load(name):
         return json.load(fh)
 
 
-def scheme_from(n_slots, factors, levels=6, q_bits=50):
-    rp = make_params(n_slots, factors, levels=levels, q_bits=q_bits)
+def scheme_from(n_slots, factors, levels=6, q_bits=50, seed=None):
+    rp = make_params(n_slots, factors, levels=levels, q_bits=q_bits, seed=seed)
     return SchemeParams(n_slots=n_slots, t=math.prod(factors), t_factors=tuple(factors), rlwe=rp)
 
 
@@ -50,11 +50,11 @@ def replay(ctx, case, encrypt=None):
     return ct
 
 
-def network_from_fixture(fx, scheme=None):
+def network_from_fixture(fx, scheme=None, seed=None):
     w, h, c = fx["input_shape"]
     layers = tuple(LayerSpec(**l) for l in fx["layers"])
     if scheme is None:
-        scheme = scheme_from(fx["n_slots"], fx["t_factors"])
+        scheme = scheme_from(fx["n_slots"], fx["t_factors"], seed=seed)
     net = NetworkSpec(scheme, TensorShape(w, h, c), layers)
     ws = WeightSet()
     for name, v in fx["weights"].items():

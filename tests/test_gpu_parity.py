@@ -224,10 +224,10 @@ def test_pinned_async_encrypt_decrypt_match_sync(golden_lib, cuda_lib):
     s = _rand_slots(P, R, rng)
     pin_in = torch.from_numpy(s.view(np.int64)).pin_memory().numpy().view(np.uint64)
     pin_out = torch.empty(s.shape, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-    cts = [gp.encrypt(pin_in[:, r:r + 2], nonce=100 + r) for r in range(0, R, 2)]
+    cts = [gp.encrypt(pin_in[:, r:r + 2], nonce=100 + r, async_=True) for r in range(0, R, 2)]
     rs = gp.rotate_many(cts, 9)
     for r, c in zip(range(0, R, 2), rs):
-        gp.decrypt(c, out=pin_out[:, r:r + 2])
+        gp.decrypt(c, out=pin_out[:, r:r + 2], async_=True)
     gp.sync()
     for r, c in zip(range(0, R, 2), cts):
         ref = gp.encrypt(np.ascontiguousarray(s[:, r:r + 2]), nonce=100 + r)

@@ -37,10 +37,10 @@ def _worker(rank, world, port, out_path, golden_path):
     from paper_2102_03494_b200.hesim import HeContext
     from paper_2102_03494_b200.planner import build_plan
     from paper_2102_03494_b200.runner import run_encrypted
-    from paper_2102_03494_b200.shard import gather_logits, scatter_packed
+    from paper_2102_03494_b200.shard import gather_logits, scatter_packed, shared_seed
     from _shared import load, network_from_fixture
     fx = load("networks.json")[0]
-    net, ws = network_from_fixture(fx)
+    net, ws = network_from_fixture(fx, seed=shared_seed(rank, world))
     plan = build_plan(net, "explicit")
     images = np.concatenate([np.array(fx["inputs"])] * world)        # 2 images per rank
     ctx = HeContext(net.scheme, batch=2, lib=Library(golden_path))
@@ -54,11 +54,44 @@ def _worker(rank, world, port, out_path, golden_path):
     dist.destroy_process_group()
 
 
-def test_two_ranks_gloo(tmp_path, golden_lib):
+@pytest.mark.parametrize("world", [2, 4])
+def test_ranks_gloo(world, tmp_path, golden_lib):
     out = tmp_path / "logits.json"
-    port = 29500 + os.getpid() % 1000
-    mp.spawn(_worker, args=(2, port, str(out), golden_lib.path), nprocs=2, join=True)
+    port = 29500 + (os.getpid() * 7 + world) % 1000
+    mp.spawn(_worker, args=(world, port, str(out), golden_lib.path), nprocs=world, join=True)
     from _shared import load
     fx = load("networks.json")[0]
     got = json.loads(out.read_text())
-    assert got == fx["logits"] * 2
+    assert got == fx["logits"] * world
+
+
+def _mismatch_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2102_03494_b200.shard import check_shared_keys
+
+    class _Ev:
+        class params:
+            seed = 1000 + rank
+
+    class _Ctx:
+        evaluator = _Ev()
+
+    try:
+        check_shared_keys(_Ctx(), world)
+        msg = "no error"
+    except ValueError as e:
+        msg = str(e)
+    if rank == 0:
+        with open(out_path, "w") as fh:
+            fh.write(msg)
+    dist.destroy_process_group()
+
+
+def test_ranks_with_different_key_seeds_are_rejected(tmp_path):
+    out = tmp_path / "msg.txt"
+    port = 28500 + os.getpid() % 1000
+    mp.spawn(_mismatch_worker, args=(2, port, str(out)), nprocs=2, join=True)
+    assert "different key seeds" in out.read_text()
