@@ -185,3 +185,65 @@ def crt_primes_for_bound(n_slots: int, magnitude_bits: float, prime_bits: int) -
         if total > magnitude_bits + 1:
             return out
     raise ValueError("bound too large")
+
+
+def _rho(n: int, budget: int) -> int | None:
+    """One nontrivial factor of composite n by Pollard-Brent rho, or None after
+    `budget` iterations."""
+    import math as _m
+    if n % 2 == 0:
+        return 2
+    for c in range(1, 20):
+        y, m, g, r, q = 2, 128, 1, 1, 1
+        x = ys = 2
+        it = 0
+        while g == 1 and it < budget:
+            x = y
+            for _ in range(r):
+                y = (y * y + c) % n
+            k = 0
+            while k < r and g == 1:
+                ys = y
+                for _ in range(min(m, r - k)):
+                    y = (y * y + c) % n
+                    q = q * abs(x - y) % n
+                g = _m.gcd(q, n)
+                k += m
+            it += r
+            r *= 2
+        if g == n:
+            g = 1
+            while g == 1:
+                ys = (ys * ys + c) % n
+                g = _m.gcd(abs(x - ys), n)
+        if 1 < g < n:
+            return g
+    return None
+
+
+def factor_plaintext_modulus(t: int, n_slots: int, budget: int = 1 << 22) -> tuple[int, ...]:
+    """Prime factors of a plaintext modulus for plaintext CRT, each checked to be
+    batching-compatible (prime, = 1 mod 4 n_slots, < 2^61).  The reference's
+    SchemeParams keeps only the product (netspec.py:116-121 multiplies the listed
+    factors), so a drop-in context has to recover them; factors of up to ~40 bits
+    are found quickly, larger ones should be passed explicitly."""
+    out, todo = [], [int(t)]
+    while todo:
+        x = todo.pop()
+        if x == 1:
+            continue
+        if is_prime(x):
+            out.append(x)
+            continue
+        f = _rho(x, budget)
+        if f is None:
+            raise ValueError(f"could not factor the plaintext modulus {t}; pass its prime factors (t_factors)")
+        todo += [f, x // f]
+    out.sort()
+    for f in out:
+        if not batching_compatible(f, n_slots):
+            raise ValueError(f"plaintext modulus factor {f} does not admit SIMD batching over {n_slots} slots "
+                             f"(needs a prime = 1 mod {4 * n_slots} below 2^61)")
+    if len(set(out)) != len(out):
+        raise ValueError(f"plaintext modulus {t} has a repeated prime factor; CRT needs distinct primes")
+    return tuple(out)

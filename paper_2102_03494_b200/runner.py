@@ -117,21 +117,25 @@ def static_bounds(net: NetworkSpec, ws: WeightSet, input_bound: int) -> list[int
 # at t = 30 bits the cfg0 chain measured fresh 35, dot+rotate-and-sum 43, slot
 # mask 32, assembly chain 6, 1x1 scalar stage 4, combine 2-6, square 41 bits.
 # Each term below is the measurement + 1 bit; 12 bits of margin on top.
-def _noise_bits(plan: PackingPlan, t_bits: float, mask_fc: bool) -> float:
+def _noise_bits(plan: PackingPlan, t_bits: float, mask_fc: bool, plain_conv_conv: bool = False) -> float:
+    """plain_conv_conv: the column stage multiplies by a masked constant plaintext
+    (the reference engine, engine.py:189-195) instead of a scalar (engine.conv_conv
+    here): about a slot mask's noise per stage instead of a few bits."""
     dot, mask, chain, square = t_bits + 14, t_bits + 3, 7, t_bits + 12
+    cols = mask + 4 if plain_conv_conv else 5
     need = t_bits + 6                                 # fresh encryption
     for k, step in enumerate(plan.steps):
         op = step.op
         if op == CONV_DENSE or (op == FFCONV and step.pattern in ("DP-HI2C-CP", "DP-DP")):
             need += dot + mask + chain
         if op == FFCONV:
-            need += 5                                     # 1x1 stage (scalar weights)
+            need += cols                                  # 1x1 stage
             if step.pattern in ("CP-HI2C-CP", "CP-HI2C-DP"):
-                need += 5
+                need += cols
             if step.pattern == "DP-DP":
                 need += dot + mask + chain
         if op == CONV_COLUMNS:
-            need += 8
+            need += cols + 3
         if op in (HIM2COL_DENSE, HIM2COL_CONV, GROUP_DENSE):
             need += mask + chain
         if op == SQUARE:

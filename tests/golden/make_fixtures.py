@@ -13,6 +13,8 @@ GPU box, so tests only ever read the committed fixtures:
                         test-strategy shape, tests/conftest.py:68-125) with
                         weights, inputs, plan steps, measured report rows,
                         depths, run_reference layer outputs and logits
+  networks_extra.json   the same record for hand-picked networks covering
+                        avg-pool, DP-DP and in-network HIm2Col steps
   cfg0.npz / cfg0.json  BASELINE configs[0]: the FFConv MNIST network on
                         seeded synthetic images: weights, inputs, reference
                         logits, count-only report, and the reference's own
@@ -192,6 +194,68 @@ def networks(count=14, seed=23, n_slots=64):
     return out
 
 
+# Hand-picked networks for the plan steps the random ones never produce: avg-pool
+# (engine.py:271-279), DP-DP, an in-network HIm2Col from a dense layout, and a
+# pooled CP -> DP chain (lola-default gives DP-DP twice around the pool).
+EXTRA_NETWORKS = [
+    ("avgpool-dense", "explicit", (6, 6, 1), [
+        dict(kind="conv", d=2, stride=1, out_channels=2, packing_hint="dense"), dict(kind="avgpool", d=2, stride=2),
+        dict(kind="square"), dict(kind="fc", out_channels=3)]),
+    ("dp-dp", "explicit", (6, 5, 2), [
+        dict(kind="ffconv", d=3, stride=1, out_channels=3, rank=2, packing_hint="dp-dp"), dict(kind="square"),
+        dict(kind="fc", out_channels=2)]),
+    ("him2col-dense", "explicit", (7, 7, 1), [
+        dict(kind="conv", d=2, stride=1, out_channels=2, packing_hint="dense"),
+        dict(kind="conv", d=2, stride=1, out_channels=2, packing_hint="conv"), dict(kind="square"),
+        dict(kind="fc", out_channels=3)]),
+    ("cp-avgpool-dp", "explicit", (7, 7, 2), [
+        dict(kind="ffconv", d=2, stride=1, out_channels=3, rank=2, packing_hint="cp-hi2c-cp"), dict(kind="square"),
+        dict(kind="avgpool", d=2, stride=2),
+        dict(kind="ffconv", d=2, stride=1, out_channels=2, rank=1, packing_hint="dp-hi2c-cp"),
+        dict(kind="fc", out_channels=2)]),
+    ("cp-avgpool-dp-lola", "lola-default", (7, 7, 2), [
+        dict(kind="ffconv", d=2, stride=1, out_channels=3, rank=2, packing_hint="cp-hi2c-cp"), dict(kind="square"),
+        dict(kind="avgpool", d=2, stride=2),
+        dict(kind="ffconv", d=2, stride=1, out_channels=2, rank=1, packing_hint="dp-hi2c-cp"),
+        dict(kind="fc", out_channels=2)]),
+    ("conv-avgpool-him2col", "explicit", (8, 8, 1), [
+        dict(kind="conv", d=3, stride=1, out_channels=2, packing_hint="conv"), dict(kind="avgpool", d=2, stride=2),
+        dict(kind="conv", d=2, stride=1, out_channels=2, packing_hint="conv"), dict(kind="square"),
+        dict(kind="fc", out_channels=2)]),
+]
+
+
+def networks_extra(seed=29, n_slots=256):
+    rng = np.random.default_rng(seed)
+    out = []
+    for name, strategy, (w, h, c), layer_docs in EXTRA_NETWORKS:
+        layers = tuple(LayerSpec(**d) for d in layer_docs)
+        shape = TensorShape(w=w, h=h, c=c)
+        prov = NetworkSpec(scheme=SchemeParams(n_slots=n_slots, t=(1 << 61)), input_shape=shape, layers=layers)
+        ws = random_weights(prov, rng, bound=3)
+        bound = max(e.static_bound for e in ref_runner.static_bounds(prov, ws, input_bound=7))
+        fs = crt_t(n_slots, bound)
+        net = NetworkSpec(scheme=SchemeParams(n_slots=n_slots, t=math.prod(fs)), input_shape=shape, layers=layers)
+        plan = build_plan(net, strategy)
+        xs = rng.integers(0, 8, size=(2, c, h, w))
+        logits, per_img_layers, res = [], [], None
+        for x in xs:
+            res = ref_runner.run_encrypted(net, plan, ws, x, capture_layers=True)
+            assert res.logits.tolist() == res.reference_logits.tolist()
+            logits.append([int(v) for v in res.logits])
+            _, ref_layers, _ = ref_runner.run_reference(net, ws, x)
+            per_img_layers.append([np.asarray(t, dtype=object).astype(str).tolist() for t in ref_layers])
+        out.append({
+            "name": name, "strategy": strategy,
+            "n_slots": n_slots, "t_factors": fs, "input_shape": [w, h, c], "layers": layer_docs,
+            "weights": _ws_json(ws), "inputs": xs.tolist(),
+            "plan": [[s.op, s.layer_index, s.pattern] for s in plan.steps],
+            "rows": _rows_json(res.report), "depth": res.depth, "assembly_depth": res.assembly_depth,
+            "logits": logits, "layer_outputs": per_img_layers,
+        })
+    return out
+
+
 # ------------------------------------------------------------------ cfg0
 def cfg0(images=2, seed=20210205):
     rng = np.random.default_rng(seed)
@@ -312,10 +376,16 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["cfg3"]:
         cfg3()
         sys.exit(0)
+    if sys.argv[1:] == ["extra"]:
+        with open(os.path.join(HERE, "networks_extra.json"), "w") as fh:
+            json.dump(networks_extra(), fh)
+        sys.exit(0)
     with open(os.path.join(HERE, "hesim_sequences.json"), "w") as fh:
         json.dump(hesim_sequences(), fh)
     with open(os.path.join(HERE, "networks.json"), "w") as fh:
         json.dump(networks(), fh)
+    with open(os.path.join(HERE, "networks_extra.json"), "w") as fh:
+        json.dump(networks_extra(), fh)
     cfg0()
     cfg3()
     weight_file()

@@ -116,3 +116,19 @@ def test_h_im2col_moves_hoisted_on_gpu(cuda_lib, golden_lib):
         words.append([ctx.evaluator.read(c.handle) for c in cols.cts])
     for a, b in zip(*words):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_extra_networks_on_gpu(cuda_lib, golden_lib, idx):
+    """avg-pool (engine.py:271-279), DP-DP and in-network HIm2Col plans on the B200:
+    the reference's logits, counts, depths and per-layer tensors, and the golden
+    model's ciphertext words."""
+    from test_host_stack import _check_network
+    fx = load("networks_extra.json")[idx]
+    sch = scheme_from(fx["n_slots"], fx["t_factors"], levels=8)
+    res = _check_network(fx, HeContext(sch, batch=2, lib=cuda_lib))
+    gold = _check_network(fx, HeContext(sch, batch=2, lib=golden_lib))
+    ev = res.value.cts[0]._ctx.evaluator
+    evg = gold.value.cts[0]._ctx.evaluator
+    for a, b in zip(res.value.cts, gold.value.cts):
+        assert np.array_equal(ev.read(a.handle), evg.read(b.handle))
