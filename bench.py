@@ -105,6 +105,16 @@ def rotation_params():
     return RlweParams(log_n=14, q=tuple(q), p=tuple(p), t=(t,), b=(), seed=CFG1["seed"])
 
 
+def rotation_config(world: int) -> dict:
+    """configs[1] workload identity, printed by both arms."""
+    P = rotation_params()
+    return {"workload": "configs[1] primitive microbench: 1024 ciphertexts per GPU, one seeded rotation "
+                        "step per batch", "ring_n": P.n, "L": P.L, "K": 1, "dnum": P.L,
+            "q_bits": [round(math.log2(x), 2) for x in P.q], "t": P.t[0], "batch_per_gpu": CFG1["batch"],
+            "rotation_step": rotation_step(), "l2": "inputs 1 GiB per batch > 126 MB L2 (no flush needed)",
+            "parallelism": f"dp{world} (independent ciphertexts, no collective)"}
+
+
 def algorithmic_counts(n: int, l: int):
     """Per-ciphertext algorithmic modmuls / bytes per kernel of one key-switched
     rotation (hybrid KS, one prime per digit, one special prime)."""
@@ -112,7 +122,7 @@ def algorithmic_counts(n: int, l: int):
     w = 8
     return {
         "k_rot_gather_intt": (l * ntt, (2 * l * n + 2 * l * n + l * n) * w),
-        "k_modup": (l * l * ntt, (l * l * n + l * l * n) * w),
+        "k_modup": (l * l * ntt, (l * n + l * l * n) * w),          # read the l digits, write l^2 extended rows
         "k_ks_inner": (2 * l * l * n, (l * l * n + 2 * l * n) * w),
         "k_ks_special": (2 * ntt + 2 * l * n, (2 * l * n + 2 * n) * w),
         "k_rescale(moddown)": (2 * l * ntt + 2 * l * n, (2 * n + 2 * l * n + l * n + 2 * l * n) * w),
@@ -149,25 +159,35 @@ def parse_prof(text: str):
 
 # ------------------------------------------------------------- CPU baselines
 def _cpu_rotations(args):
-    """Reference algorithm (slot oracle) rotations over `count` slot vectors."""
+    """Reference algorithm (slot oracle) rotations over `count` slot vectors, by the
+    configs[1] step.  The vectors are encrypted before the timer starts; only the
+    rotations are timed (in this process)."""
     count, reps, seed = args
     from oracle.slot_oracle import Params, SlotContext
     ctx = SlotContext(Params(CFG1["n_slots"], CFG1["t"]))
     rng = np.random.default_rng(seed)
     cts = [ctx.encrypt(rng.integers(-1, 2, size=CFG1["n_slots"])) for _ in range(count)]
-    k = int(rng.integers(1, CFG1["n_slots"]))
+    k = rotation_step()
     t0 = time.perf_counter()
     for _ in range(reps):
         cts = [ctx.rotate(c, k) for c in cts]
     return count * reps, time.perf_counter() - t0
 
 
+def rotation_step() -> int:
+    """The configs[1] step: one seeded k in [1, 8192) per batch (same for both arms)."""
+    return int(np.random.default_rng(CFG1["seed"]).integers(1, CFG1["n_slots"]))
+
+
 def cpu_baseline_rotation(cores: int = 1, seconds: float = 2.0):
+    """rotations/s of the reference algorithm over the configs[1] batch on `cores`
+    processes: each worker rotates its share of the 1024 vectors `reps` times and
+    times itself; rate = all rotations / the slowest worker's rotation time."""
     # calibrate reps so the sample is a bounded amount of CPU work
     n, dt = _cpu_rotations((64, 1, 1))
     per = dt / n
     count = CFG1["batch"]
-    reps = max(1, int(seconds / max(per * count, 1e-9)))
+    reps = max(1, int(seconds * max(1, cores) / max(per * count, 1e-9)))
     if cores <= 1:
         done, el = _cpu_rotations((count, reps, 7))
         rate = done / el
@@ -175,11 +195,10 @@ def cpu_baseline_rotation(cores: int = 1, seconds: float = 2.0):
         import multiprocessing as mp
         chunk = max(1, count // cores)
         with mp.Pool(cores) as pool:
-            t0 = time.perf_counter()
             res = pool.map(_cpu_rotations, [(chunk, reps, 7 + i) for i in range(cores)])
-            el = time.perf_counter() - t0
-        rate = sum(r[0] for r in res) / el
-    return rate, f"{count} slot vectors x {reps} rotation rounds (N=8192, t=1099511922689)"
+        rate = sum(r[0] for r in res) / max(r[1] for r in res)
+    return rate, (f"{count} slot vectors x {reps} rotation rounds by k = {rotation_step()} (N=8192, "
+                  f"t=1099511922689), {max(1, cores)} worker process(es), vectors built before the timer")
 
 
 # --------------------------------------------------------------- our arm
@@ -201,7 +220,7 @@ def run_rotation(args, rank, world, local_rank):
     rng = np.random.default_rng(CFG1["seed"] + rank)
     slots = np.mod(rng.integers(-1, 2, size=(1, B, n)), P.t[0]).astype(np.uint64)
     ct = ev.encrypt(slots)
-    k = int(np.random.default_rng(CFG1["seed"]).integers(1, P.n_slots))
+    k = rotation_step()
     pt = ev.encode(np.mod(rng.integers(-1, 2, size=(1, n)), P.t[0]).astype(np.uint64))
     ev.keygen_rotations([k])
     ev.sync()
@@ -328,11 +347,7 @@ def run_rotation(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic (seeded slot values uniform in {-1,0,1})",
-        "config": {"workload": "configs[1] primitive microbench: 1024 ciphertexts per GPU, one seeded rotation "
-                               "step per batch", "ring_n": n, "L": P.L, "K": 1, "dnum": P.L,
-                   "q_bits": [round(math.log2(x), 2) for x in P.q], "t": P.t[0], "batch_per_gpu": B,
-                   "rotation_step": k, "l2": "inputs 1 GiB per batch > 126 MB L2 (no flush needed)",
-                   "parallelism": f"dp{world} (independent ciphertexts, no collective)"},
+        "config": rotation_config(world),
         "rates": {
             "rotations_per_s": rot_rate,
             "hma_per_s": world * B * args.steps / (hma_ms * 1e-3),
@@ -682,18 +697,36 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
-    first_logits = None
+    round_logits = []
     for k in range(rounds):
         res = run_encrypted(net, plan, ws, None, ctx=ctx, packed=scatter_round(k), decrypt=False)
         lg = gather_logits(ctx, res.value, rank, world, device) if world > 1 else _decrypt_logits(res, ctx)
-        if first_logits is None:
-            first_logits = lg
+        round_logits.append(lg)
     ev.sync()
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # every image's decrypted logits against the oracle (the reference's direct-loop
+    # network, runner.py:197-226 restated in oracle/slot_oracle.py), on rank 0
+    check = None
+    if rank == 0:
+        got = {}
+        for k, lg in enumerate(round_logits):
+            lg = np.atleast_2d(lg)
+            for r in range(world):
+                a, b = shard_range(images_total, r, world)
+                for j in range(chunk):
+                    idx = a + k * chunk + j
+                    if idx < b:
+                        got[idx] = [int(v) for v in lg[r * chunk + j]]
+        want = _oracle_logits(net, ws, xs_all)
+        bad = [i for i in range(images_total) if got.get(i) != want[i]]
+        check = {"images_checked": len(got), "logits_match": not bad and len(got) == images_total,
+                 "mismatched_images": bad[:8],
+                 "oracle": "oracle/slot_oracle.run_reference_ints (reference runner.py:197-226 restated)"}
+    first_logits = round_logits[0] if round_logits else None
     # per-kernel breakdown of one chunk (single-stream, isolated kernel times)
     lib.call("fhe_prof_enable", ev.ctx, 1)
     evaluate(packed[:1])
@@ -722,9 +755,21 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
         "gpu_launches": int(cnt1.value - cnt0.value),
         "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": int(10 * images_total * 8 * rp.T),
         "clocks": clk.summary(),
-        "logits_sample": [str(int(v)) for v in np.asarray(first_logits)[0][:3]] if first_logits is not None else None,
+        "logits_sample": [str(int(v)) for v in np.atleast_2d(first_logits)[0][:3]] if first_logits is not None else None,
+        "logits_check": check,
         "kernel_ms_one_chunk": breakdown,
     }
+
+
+def _oracle_logits(net, ws, xs):
+    """Reference logits of every image (object ints) from the oracle's direct loops."""
+    from oracle.slot_oracle import run_reference_ints
+    layers = [{k: v for k, v in l.__dict__.items() if v is not None} for l in net.layers]
+    wd = {}
+    for name in ws.names():
+        i, key = name[len("layer"):].split(".")
+        wd.setdefault(int(i), {})[key] = ws[name].values
+    return [[int(v) for v in run_reference_ints(layers, wd, x)[0]] for x in xs]
 
 
 def _decrypt_logits(res, ctx):
@@ -827,8 +872,10 @@ def run_reference_arm(args, rank, world):
         "value": v, "unit": "rotations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * CFG1["batch"] / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": "configs[1] primitive microbench (reference slot-engine algorithm, np.roll)"},
-        "cpu_baseline": {"value": v, "unit": "rotations/s", "cores": cores, "kind": "port", "sample": sample},
+        "config": rotation_config(world),
+        "cpu_baseline": {"value": v, "unit": "rotations/s", "cores": cores, "kind": "port", "sample": sample,
+                         "algorithm": "reference slot engine (oracle/slot_oracle.py restates hesim.py:244-261): "
+                                      "np.roll of an int64 slot vector"},
         "e2e": {"value": v, "unit": "rotations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference is a slot simulator: its rotation is np.roll, not a key-switched RLWE rotation",
     }
@@ -912,16 +959,17 @@ def main():
         return
     res = run_rotation(args, rank, world, local_rank)
     if not args.no_inference:
-        # secondary line item: configs[2]-shaped inference on a bounded sample per GPU
-        inf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=2, warmup=1,
+        # secondary line item: configs[2], the full 256-image batch sharded over the ranks,
+        # one timed step, every image's logits checked against the oracle
+        inf = run_inference(args, rank, world, local_rank, images_total=256, steps=1, warmup=1,
                             schedule="reference")
         res["inference"] = inf
         res["rates"]["images_per_s"] = inf["images_per_s"]
-        hinf = run_inference(args, rank, world, local_rank, images_total=32 * world, steps=2, warmup=1,
+        hinf = run_inference(args, rank, world, local_rank, images_total=256, steps=1, warmup=1,
                              schedule="hoisted")
         res["inference_hoisted"] = {k: hinf[k] for k in ("schedule", "images_per_s", "e2e_images_per_s",
                                                          "logical_rotations_per_chunk", "roofline",
-                                                         "kernel_ms_one_chunk")}
+                                                         "kernel_ms_one_chunk", "logits_check")}
         res["rates"]["images_per_s_hoisted"] = hinf["images_per_s"]
     if rank == 0 and world == 1:
         rate, sample = cpu_baseline_rotation(1, seconds=3.0)

@@ -138,6 +138,9 @@ int fhe_pt_read(fhe_ctx *ctx, const fhe_pt *pt, uint64_t *words);
  * valid only after fhe_sync().  Pageable buffers are copied synchronously. */
 int fhe_encrypt(fhe_ctx *ctx, const uint64_t *slots, uint32_t nonce, fhe_ct *out);
 int fhe_decrypt(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *slots);
+/* slots [lo, lo + cnt) of both batching rows only: out [T*R][2][cnt] residues mod t_k
+ * (the logits of a network sit in slot 0; the full decrypt moves T*R*n words) */
+int fhe_decrypt_slots(fhe_ctx *ctx, const fhe_ct *ct, uint32_t lo, uint32_t cnt, uint64_t *out);
 /* Deferred checks (no host synchronization on the evaluation path):
  * fhe_check_zero_tail enqueues the rotate_and_sum precondition of the reference
  * (hesim.py:360-361: every slot at index >= m is zero) for every physical

@@ -745,6 +745,19 @@ int fhe_decrypt(fhe_ctx *c, const fhe_ct *ct, uint64_t *slots) {
     return 0;
 }
 
+int fhe_decrypt_slots(fhe_ctx *c, const fhe_ct *ct, uint32_t lo, uint32_t cnt, uint64_t *out) {
+    if ((u64)lo + cnt > c->N) return fail(FHE_EINVAL, "decrypt_slots: [%u, %u) exceeds %u slots", lo, lo + cnt, c->N);
+    u64 *coef = (u64 *)malloc(c->n * 8), *slots = (u64 *)malloc(c->n * 8);
+    for (u32 ci = 0; ci < ct->count; ci++) {
+        decrypt_one(c, ct, ci, coef);
+        coef_to_slots(c, ci / ct->R, coef, slots);
+        for (u32 r = 0; r < 2; r++)
+            for (u32 x = 0; x < cnt; x++) out[((size_t)ci * 2 + r) * cnt + x] = slots[r * c->N + lo + x];
+    }
+    free(coef); free(slots);
+    return 0;
+}
+
 int fhe_check_zero_tail(fhe_ctx *c, const fhe_ct *ct, uint32_t m) {
     if (m > c->N) return fail(FHE_EINVAL, "check_zero_tail: m = %u exceeds %u slots", m, c->N);
     if (m == c->N) return 0;

@@ -79,6 +79,7 @@ SIGNATURES = {
     "fhe_decrypt": (c_int, [c_void_p, c_void_p, _U64P]),
     "fhe_decrypt_raw": (c_int, [c_void_p, c_void_p, _U64P]),
     "fhe_check_zero_tail": (c_int, [c_void_p, c_void_p, c_uint32]),
+    "fhe_decrypt_slots": (c_int, [c_void_p, c_void_p, c_uint32, c_uint32, _U64P]),
     "fhe_status": (c_int, [c_void_p, POINTER(c_uint32), POINTER(c_uint32), c_int]),
     "fhe_add": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "fhe_mul_plain": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

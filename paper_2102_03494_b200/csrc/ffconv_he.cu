@@ -19,6 +19,7 @@
 
 #include "ffconv_he.h"
 #include "kernels.cuh"
+#include "ks_fused.cuh"
 #include "ntt4.cuh"
 
 // =================================================================== errors
@@ -1177,6 +1178,21 @@ extern "C" int fhe_decrypt(fhe_ctx *c, const fhe_ct *ct, uint64_t *slots) {
     return 0;
 }
 
+extern "C" int fhe_decrypt_slots(fhe_ctx *c, const fhe_ct *ct, uint32_t lo, uint32_t cnt, uint64_t *out) {
+    if ((u64)lo + cnt > c->N) return fail(FHE_EINVAL, "decrypt_slots: [%u, %u) exceeds %u slots", lo, lo + cnt, c->N);
+    if (!cnt) return 0;
+    size_t n = c->n, l = ct->level, nct = ct->count;
+    TRY(ensure_tmp(c, nct * n * (l + 1) + nct * 2 * cnt));
+    u64 *X = c->w_tmp, *m = X + nct * l * n, *o = m + nct * n;
+    TRY(decode_ntt_order(c, ct, X, m));
+    const long long total = (long long)nct * 2 * cnt;
+    EW(k_gather_slot_range, total, m, o, total, (int)c->logn, lo, cnt, c->d_slot2ntt);
+    CHECK_LAUNCH();
+    CU(cudaMemcpyAsync(out, o, total * 8, cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    return 0;
+}
+
 extern "C" int fhe_check_zero_tail(fhe_ctx *c, const fhe_ct *ct, uint32_t m) {
     if (m > c->N) return fail(FHE_EINVAL, "check_zero_tail: m = %u exceeds %u slots", m, c->N);
     if (m == c->N) return 0;
@@ -1404,7 +1420,82 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     return 0;
 }
 
+// ModUp fused into the key inner product (ks_fused.cuh): extended digits stay on
+// chip, accumulators in TMEM; then the ModDown rescale.  Single-CTA rows of
+// 2^9 .. 2^14 words, digits read in natural order (not the hoisted Ext path).
+template <int LOGN>
+static void launch_ks_fused(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsAdd &kad) {
+    using F = KsfCfg<LOGN>;
+    const size_t smem = (size_t)F::C::SMEM_WORDS * sizeof(u64);
+    {
+        std::lock_guard<std::mutex> lk(g_attr_mu);
+        if (!g_attr_done.count((const void *)k_ks_fused<LOGN>)) {
+            cudaFuncSetAttribute((const void *)k_ks_fused<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            g_attr_done.insert((const void *)k_ks_fused<LOGN>);
+        }
+    }
+    ProfScope ps_(c, "k_ks_fused");
+    k_ks_fused<LOGN><<<(unsigned)(S * (l + 1)), F::TH, smem, c->st>>>(dt, c->w_Acc, S, (int)l, (int)c->L, c->special_id,
+                                                                    c->d_mods, kad);
+}
+
+// FHE_KS_FUSED=1 selects the fused path.  Off by default: bit-exact, but measured slower
+// at configs[1] (127 K vs 150 K rotations/s) -- the TMEM accumulators
+// hold 64 bits per word, so every product needs its own Montgomery reduction, where
+// k_ks_inner accumulates l products in 128 bits and reduces once.
+static bool ks_fused_ok(const fhe_ctx *c) {
+    const char *e = getenv("FHE_KS_FUSED");
+    return e && atoi(e) && c->logn >= 9 && c->logn <= 14;
+}
+
+static int keyswitch_fused(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsOut &ko) {
+    const size_t n = c->n;
+    KsAdd kad;
+    memset(&kad, 0, sizeof kad);
+    for (int s = 0; s < S; s++) { kad.add[s] = ko.add[s]; kad.add_g[s] = ko.add_g[s]; kad.acc[s] = ko.acc[s]; }
+    kad.add_pstride = ko.add_pstride;
+    kad.acc_pstride = ko.acc_pstride;
+    kad.add_pmask = ko.add_pmask;
+    for (u32 i = 0; i < l; i++) kad.pr[i] = c->pmont[i];
+    // l^2 ModUp transforms + 2 special-prime inverses per ciphertext, key inner product + ModDown scaling
+    c->alg_mm += (double)S * ((double)(l * l + 2) * (n / 2) * c->logn + (2.0 * l * (l + 1) + 2.0 * l) * n);
+    switch (c->logn) {
+        case 9: launch_ks_fused<9>(c, S, l, dt, kad); break;
+        case 10: launch_ks_fused<10>(c, S, l, dt, kad); break;
+        case 11: launch_ks_fused<11>(c, S, l, dt, kad); break;
+        case 12: launch_ks_fused<12>(c, S, l, dt, kad); break;
+        case 13: launch_ks_fused<13>(c, S, l, dt, kad); break;
+        case 14: launch_ks_fused<14>(c, S, l, dt, kad); break;
+        default: return fail(FHE_EINVAL, "fused key switching needs 2^9 <= n <= 2^14");
+    }
+    CHECK_LAUNCH();
+    // the special prime's accumulators to coefficient form, in place: row r = (s, p)
+    InttRowsArgs ia = iargs(c->w_Acc + (size_t)l * n, c->w_Acc + (size_t)l * n, 0);
+    ia.rdiv = 2;
+    ia.sA = ia.dA = (long long)2 * (l + 1) * n;
+    ia.sB = ia.dB = (long long)(l + 1) * n;
+    ia.map.id[0] = (unsigned char)c->special_id;
+    c->alg_mm -= (double)2 * S * (n / 2) * c->logn;            // counted above
+    TRY(intt_rows(c, 2 * S, ia, "k_intt_rows(ks_special)"));
+    RescaleArgs ra;
+    memset(&ra, 0, sizeof ra);
+    for (int s = 0; s < S; s++) {
+        ra.coef[s] = c->w_Acc + ((size_t)s * 2 * (l + 1) + l) * n;
+        ra.base[s] = c->w_Acc + (size_t)s * 2 * (l + 1) * n;
+        ra.out[s] = ko.out[s];
+    }
+    ra.coef_pstride = (long long)(l + 1) * n;
+    ra.base_pstride = (long long)(l + 1) * n;
+    ra.out_pstride = ko.out_pstride;
+    ra.src_id = c->special_id;
+    for (u32 i = 0; i < l; i++) { ra.fac[i] = c->pinv[i]; ra.fac_sh[i] = c->pinv_sh[i]; }
+    LOGN_SWITCH(c->logn, launch_row<LG, false, RescaleW<LG>::value>(c, "k_rescale(moddown)", k_rescale<LG>, dim3(S, 2, l), c->st, ra, c->d_mods));
+    CHECK_LAUNCH();
+    return 0;
+}
+
 static int keyswitch_core(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsOut &ko) {
+    if (ks_fused_ok(c)) return keyswitch_fused(c, S, l, dt, ko);
     TRY(keyswitch_modup(c, S, l, dt));
     return keyswitch_tail(c, S, l, dt, ko);
 }
@@ -1424,9 +1515,22 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
     std::vector<const u64 *> keys(in.size());
     size_t n = c->n;
     // (profiling runs single-stream so every kernel is timed in isolation)
-    const bool two = in.size() > (size_t)c->S && !c->prof && c->lanes > 1;
     // balanced sub-batches: ceil(count / ceil(count / S)) instead of S + remainder
-    const size_t nsub = (in.size() + c->S - 1) / c->S;
+    size_t Smax = c->S;
+    if (ks_fused_ok(c) && !getenv("FHE_KS_BATCH")) {
+        // fused path: one CTA per (ciphertext, prime), S (l + 1) CTAs per launch -- the
+        // largest S whose launch fills whole waves of the SMs best
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
+        double best = 0;
+        for (int s = c->S; s >= std::max(1, c->S / 2); s--) {
+            const int blocks = s * (int)(l + 1), waves = (blocks + sms - 1) / sms;
+            const double eff = (double)blocks / ((double)waves * sms);
+            if (eff > best + 0.02) { best = eff; Smax = (size_t)s; }
+        }
+    }
+    const bool two = in.size() > Smax && !c->prof && c->lanes > 1;
+    const size_t nsub = (in.size() + Smax - 1) / Smax;
     const size_t SB = (in.size() + nsub - 1) / nsub;
     if (two) {
         CU(cudaEventRecord(c->ev_fork, c->streams[0]));

@@ -749,6 +749,18 @@ __global__ void k_gather_slots(const u64 *__restrict__ A, u64 *__restrict__ out,
     }
 }
 
+// out[ci][r][x] = A[ci][slot2ntt[r N + lo + x]] for x < cnt: a slot range of both rows
+__global__ void k_gather_slot_range(const u64 *__restrict__ A, u64 *__restrict__ out, long long total, int logn,
+                                    u32 lo, u32 cnt, const u32 *__restrict__ slot2ntt) {
+    const long long n = 1ll << logn;
+    const u32 N = (u32)(n >> 1);
+    GRID_STRIDE(idx, total) {
+        const long long ci = idx / (2 * cnt);
+        const u32 rem = (u32)(idx % (2 * cnt)), r = rem / cnt, x = rem % cnt;
+        out[idx] = A[ci * n + slot2ntt[r * N + lo + x]];
+    }
+}
+
 // secret key: per prime id row, ternary s mod q (NTT pending)
 __global__ void k_sk_prep(u64 *__restrict__ out, long long total, int logn, u64 seed, const unsigned char *ids,
                           const ModInfo *__restrict__ mods) {

@@ -358,18 +358,41 @@ class HeContext:
         per[:, 0::2] = raw[:, : (self.batch + 1) // 2, :N]
         if self.batch > 1:
             per[:, 1::2] = raw[:, : self.batch // 2, N:]
-        fs = ev.params.t
-        if len(fs) == 1:
-            out = per[0].astype(np.int64) if self.params.int64_storage else per[0].astype(object)
-        else:
-            t = self.params.t
-            acc = np.zeros(per.shape[1:], dtype=object)
-            for f, r in zip(fs, per):
-                mf = t // f
-                acc = acc + r.astype(object) * (mf * pow(mf, -1, f))
-            acc = acc % t
-            out = acc.astype(np.int64) if self.params.int64_storage else acc
+        out = self._crt(per)
         return out[0] if self.batch == 1 else out
+
+    def _crt(self, per: np.ndarray) -> np.ndarray:
+        """(T, ...) residues mod t_i -> (...) residues mod t (int64 when t fits)."""
+        fs = self.evaluator.params.t
+        if len(fs) == 1:
+            return per[0].astype(np.int64) if self.params.int64_storage else per[0].astype(object)
+        t = self.params.t
+        acc = np.zeros(per.shape[1:], dtype=object)
+        for f, r in zip(fs, per):
+            mf = t // f
+            acc = acc + r.astype(object) * (mf * pow(mf, -1, f))
+        acc = acc % t
+        return acc.astype(np.int64) if self.params.int64_storage else acc
+
+    def decrypt_slots(self, ct: SlotCiphertext, m: int) -> np.ndarray:
+        """decrypt(ct)[..., :m] without moving or reconstructing the other slots:
+        centered values, (m,) for batch 1 else (batch, m).  The device decodes every
+        slot; only the first m of each row cross to the host and go through CRT."""
+        if not ct.tracked:
+            raise ValueError("cannot decrypt a count-only ciphertext")
+        N = self.params.n_slots
+        if not 0 <= m <= N:
+            raise ValueError(f"m must be in [0, {N}], got {m}")
+        raw = self.evaluator.decrypt_slots(ct.handle, 0, m)               # (T, R, 2, m)
+        self.check()
+        per = np.empty((raw.shape[0], self.batch, m), dtype=np.uint64)
+        per[:, 0::2] = raw[:, : (self.batch + 1) // 2, 0]
+        if self.batch > 1:
+            per[:, 1::2] = raw[:, : self.batch // 2, 1]
+        res = np.asarray(self._crt(per)).astype(object)
+        t = self.params.t
+        res[res >= (t + 1) // 2] -= t
+        return res[0] if self.batch == 1 else res
 
     # --------------------------------------------------------------- client
     def encode(self, values) -> PlainVector:

@@ -155,6 +155,12 @@ class Evaluator:
             self.sync()
         return out.reshape(self.T, ct.rows, self.n)
 
+    def decrypt_slots(self, ct: Ciphertext, lo: int, cnt: int) -> np.ndarray:
+        """Residues of slots [lo, lo + cnt) of both rows: [T][R][2][cnt] (synchronous)."""
+        out = np.empty((self.T, ct.rows, 2, cnt), dtype=np.uint64)
+        self.lib.call("fhe_decrypt_slots", self.ctx, ct.ptr, int(lo), int(cnt), u64_ptr(out))
+        return out
+
     def check_zero_tail(self, ct: Ciphertext, m: int) -> None:
         """Enqueue the rotate_and_sum precondition check (slots >= m zero); a
         violation shows up in status()."""

@@ -57,12 +57,13 @@ def shared_seed(rank: int, world: int) -> int:
 def check_shared_keys(ctx, world: int) -> None:
     """Raise unless every rank's context derives its keys from the same seed."""
     import torch.distributed as dist
-    if world <= 1:
+    if world <= 1 or getattr(ctx, "_keys_shared", False):
         return
     seeds = [None] * world
     dist.all_gather_object(seeds, int(ctx.evaluator.params.seed))
     if len(set(seeds)) != 1:
         raise ValueError("ranks use different key seeds; build every rank's parameters with shared_seed()")
+    ctx._keys_shared = True                      # checked once per context
 
 
 def _cts_of(packed):

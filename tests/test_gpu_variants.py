@@ -1,6 +1,7 @@
 """Library build-time/run-time variants stay bit-exact: the GPU parity checks of
 test_gpu_parity.py re-run in a subprocess under each environment switch the
-library reads once per process (FHE_LANES: key-switch lanes; FHE_FUSED_MODDOWN:
+library reads once per process (FHE_LANES: key-switch lanes; FHE_KS_FUSED=1: ModUp
+fused into the key inner product with TMEM accumulators; FHE_FUSED_MODDOWN:
 the q primes' inner product inside the ModDown rescale; FHE_KS_BATCH: sub-batch
 size; FHE_KS_VARIANT: inner-product thread mapping)."""
 
@@ -19,6 +20,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = [
     {"FHE_LANES": "3", "FHE_KS_BATCH": "2"},
     {"FHE_LANES": "1", "FHE_KS_BATCH": "2"},
+    # ModUp fused into the key inner product, accumulators in TMEM (ks_fused.cuh)
+    {"FHE_KS_FUSED": "1", "FHE_KS_BATCH": "2"},
+    {"FHE_KS_FUSED": "1"},
     {"FHE_FUSED_MODDOWN": "1", "FHE_KS_BATCH": "2"},
     {"FHE_KS_BATCH": "3", "FHE_KS_VARIANT": "1"},
 ]
