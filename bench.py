@@ -537,6 +537,12 @@ ABLATION = [
 ]
 
 
+# logical rotations per image of each variant in the reference's own report (SURVEY.md
+# section 8(d), configs[4]); the F4 slot-0 masks are plaintext products and add none
+REF_ROTATIONS = {"conv-dense": 10463, "conv-cp": 1173, "ffconv-r1-dp": 3031, "ffconv-r2-dp": 4889,
+                 "ffconv-r4-dp": 8605, "ffconv-r1-cp": 1173, "ffconv-r2-cp": 1173, "ffconv-r4-cp": 1173}
+
+
 def ablation_setup(first, images, seed, offset=0):
     from paper_2102_03494_b200.hesim import SchemeParams
     from paper_2102_03494_b200.netspec import LayerSpec, NetworkSpec, synthetic_weights
@@ -584,10 +590,16 @@ def run_ablation(args, rank, world, local_rank):
             torch.distributed.barrier()
         c0 = ctx.counters.copy()
         t0 = time.perf_counter()
+        results = []
         for p in packed:
             res = run_encrypted(net, plan, ws, None, ctx=ctx, packed=p, decrypt=False)
+            results.append(res)
         ctx.evaluator.sync()
         el = time.perf_counter() - t0
+        # every image's logits against the oracle (outside the timed region)
+        got = [row for r in results for row in np.atleast_2d(_decrypt_logits(r, ctx)).tolist()][:per_rank]
+        want = _oracle_logits(net, ws, xs)
+        match = [[int(v) for v in g] for g in got] == want
         if world > 1:
             t = torch.tensor([el], device=f"cuda:{local_rank}")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -598,7 +610,10 @@ def run_ablation(args, rank, world, local_rank):
                      "add_cc_per_image": d.add_cc // per_chunk, "assembly_masks_per_image": d.assembly_mul_pc // per_chunk,
                      "crt_primes": len(rp.t), "L": rp.L, "images_per_s": args.images / el,
                      "latency_ms_per_batch": 1e3 * el / per_chunk, "batch": chunk,
-                     "depth": res.depth, "assembly_depth": res.assembly_depth}
+                     "depth": res.depth, "assembly_depth": res.assembly_depth,
+                     "reference_rotations_per_image": REF_ROTATIONS[name],
+                     "logits_checked": len(want), "logits_match": match,
+                     "distinct_rotation_keys": len(ctx.rotation_steps)}
         del ctx, packed, res
     return out
 
@@ -737,7 +752,14 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     # physical ciphertext rotations: logical rotations x CRT primes x row pairs
     phys_rot = rots * rp.T * ctx.rows
     mm = mm1.value - mm0.value          # algorithmic modmuls the library issued (fhe_work_modmuls)
-    in_bytes = int(np.prod(xs_all.shape[1:]) * 8 * images_total)
+    # bytes crossing PCIe in the e2e loop: the encrypted inputs' slot residues (rank 0
+    # encrypts every rank's batch: T x R x n words per input ciphertext) and the logit
+    # slot ranges read back (fhe_decrypt_slots: T x R x 2 x m words per logit ciphertext)
+    from paper_2102_03494_b200.runner import _logits_layout
+    in_cts = 1 if plan.steps[0].op == "pack-dense" else plan.steps[0].kernel.k_columns(plan.steps[0].in_shape.c)
+    n_logit_cts, m_logit = _logits_layout(net, plan)
+    in_bytes = rounds * world * in_cts * rp.T * ctx.rows * rp.n * 8
+    out_bytes = rounds * world * n_logit_cts * rp.T * ctx.rows * 2 * m_logit * 8
     return {
         "schedule": schedule,
         "images_per_s": images_total * steps / (ms * 1e-3),
@@ -753,7 +775,7 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
                      "algorithmic": "whole evaluation: (n/2)log2(n) per row (I)NTT at the row's level, key inner "
                                     "products, ModDown scaling, hoisted-dot MACs (elementwise ops not counted)"},
         "gpu_launches": int(cnt1.value - cnt0.value),
-        "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": int(10 * images_total * 8 * rp.T),
+        "h2d_bytes_per_step": int(in_bytes), "d2h_bytes_per_step": int(out_bytes),
         "clocks": clk.summary(),
         "logits_sample": [str(int(v)) for v in np.atleast_2d(first_logits)[0][:3]] if first_logits is not None else None,
         "logits_check": check,

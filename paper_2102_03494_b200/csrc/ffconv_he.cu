@@ -1742,12 +1742,46 @@ extern "C" int fhe_hoisted_dot(fhe_ctx *c, fhe_ct *const *R, const uint32_t *g, 
     return 0;
 }
 
+// one launch per MANY same-shape items (item = blockIdx.z); a list of mixed shapes is
+// split at every shape change
 extern "C" int fhe_mul_plain_many(fhe_ctx *c, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m) {
-    for (u32 i = 0; i < m; i++) TRY(fhe_mul_plain(c, a[i], pt[i], out[i]));
+    for (u32 i = 0; i < m; i++) {
+        if (!same_shape(a[i], out[i])) return fail(FHE_ELEVEL, "mul_plain_many: shape/level mismatch at %u", i);
+        if (!pt[i]->encoded) return fail(FHE_EINVAL, "mul_plain_many: plaintext %u was never encoded", i);
+    }
+    for (u32 i0 = 0; i0 < m;) {
+        u32 i1 = i0 + 1;
+        while (i1 < m && i1 - i0 < MANY && same_shape(a[i1], a[i0])) i1++;
+        ManyTab t;
+        memset(&t, 0, sizeof t);
+        for (u32 i = i0; i < i1; i++) { t.a[i - i0] = a[i]->d; t.b[i - i0] = pt[i]->ntt_m; t.out[i - i0] = out[i]->d; }
+        const int rows = (int)(a[i0]->count * 2 * a[i0]->level);
+        const unsigned bx = (unsigned)std::max<size_t>(1, (c->n / 2 + 255) / 256);
+        dim3 grid(bx, (unsigned)std::min(rows, 65535), i1 - i0);
+        ProfScope ps_(c, "k_mul_plain");
+        k_mul_plain_many<<<grid, 256, 0, c->st>>>(t, rows, (int)a[i0]->level, (int)c->L, (int)a[i0]->R, (int)c->logn,
+                                                  c->d_mods);
+        CHECK_LAUNCH();
+        i0 = i1;
+    }
     return 0;
 }
 extern "C" int fhe_add_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *b, fhe_ct *const *out, uint32_t m) {
-    for (u32 i = 0; i < m; i++) TRY(fhe_add(c, a[i], b[i], out[i]));
+    for (u32 i = 0; i < m; i++)
+        if (!same_shape(a[i], b[i]) || !same_shape(a[i], out[i])) return fail(FHE_ELEVEL, "add_many: shape/level mismatch at %u", i);
+    for (u32 i0 = 0; i0 < m;) {
+        u32 i1 = i0 + 1;
+        while (i1 < m && i1 - i0 < MANY && same_shape(a[i1], a[i0])) i1++;
+        ManyTab t;
+        memset(&t, 0, sizeof t);
+        for (u32 i = i0; i < i1; i++) { t.a[i - i0] = a[i]->d; t.b[i - i0] = b[i]->d; t.out[i - i0] = out[i]->d; }
+        const long long total = (long long)ct_words(a[i0]);
+        const unsigned bx = (unsigned)std::max<long long>(1, std::min<long long>((total / 2 + 255) / 256, 148 * 8));
+        ProfScope ps_(c, "k_add");
+        k_add_many<<<dim3(bx, 1, i1 - i0), 256, 0, c->st>>>(t, total, (int)a[i0]->level, (int)c->logn, c->d_mods);
+        CHECK_LAUNCH();
+        i0 = i1;
+    }
     return 0;
 }
 

@@ -615,6 +615,44 @@ __global__ void k_mul_plain(const u64 *__restrict__ a, const u64 *__restrict__ p
     }
 }
 
+// Batched forms: up to MANY independent same-shape operations per launch, item =
+// blockIdx.z (one launch instead of one per ciphertext object).
+#define MANY 64
+struct ManyTab {
+    const u64 *a[MANY];
+    const u64 *b[MANY];          // plaintext (mul) or second operand (add)
+    u64 *out[MANY];
+};
+__global__ void k_mul_plain_many(const ManyTab t, int rows, int l, int L, int R, int logn,
+                                 const ModInfo *__restrict__ mods) {
+    const long long n = 1ll << logn;
+    const long long x = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+    if (x >= n) return;
+    const int it = blockIdx.z;
+    const u64 *a = t.a[it], *ptm = t.b[it];
+    u64 *out = t.out[it];
+    for (int row = blockIdx.y; row < rows; row += gridDim.y) {
+        const int i = row % l, ci = row / (2 * l), k = ci / R;
+        const ModInfo &M = mods[i];
+        const long long off = (long long)row * n + x;
+        const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(a + off);
+        const ulonglong2 w = __ldg(reinterpret_cast<const ulonglong2 *>(ptm + ((long long)k * L + i) * n + x));
+        *reinterpret_cast<ulonglong2 *>(out + off) = make_ulonglong2(mont(av.x, w.x, M.q, M.qinv), mont(av.y, w.y, M.q, M.qinv));
+    }
+}
+__global__ void k_add_many(const ManyTab t, long long total, int l, int logn, const ModInfo *__restrict__ mods) {
+    const int it = blockIdx.z;
+    const u64 *a = t.a[it], *b = t.b[it];
+    u64 *out = t.out[it];
+    for (long long idx = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); idx < total;
+         idx += 2ll * gridDim.x * blockDim.x) {
+        const u64 q = mods[(int)((u32)(idx >> logn) % (u32)l)].q;
+        const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(a + idx);
+        const ulonglong2 bv = *reinterpret_cast<const ulonglong2 *>(b + idx);
+        *reinterpret_cast<ulonglong2 *>(out + idx) = make_ulonglong2(addm(av.x, bv.x, q), addm(av.y, bv.y, q));
+    }
+}
+
 struct ScalarTab {
     u64 w[MAXQ], wsh[MAXQ];
 };

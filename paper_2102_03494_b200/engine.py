@@ -37,6 +37,7 @@ from .packing import (
     combine_to_dense,
     h_grouping,
     source_slots,
+    tree_combine,
 )
 
 
@@ -220,13 +221,13 @@ def _dense_assemble(x, w, kernel, ctx, blocks):
             dots = dots + (ctx.counters - before)
             before = ctx.counters.copy()
             masked = _mask_slot0_many(ctx, outs)
-            first = 1 if acc is None else 0
+            # the group's outputs as one contiguous block (tree: log2 keys), then placed
+            # at its offset in the block: len - 1 + 1 rotations, as the chain's
+            group, _ = tree_combine(ctx, masked, [1] * len(masked))
             if acc is None:
-                acc = masked[0]
-            moved = _rotate_multi(ctx, masked[first:], [(n - (s0 + i - b0)) % n
-                                                       for i in range(first, len(masked))])
-            for m in moved:
-                acc = ctx.add_cc(acc, m)
+                acc = group
+            else:
+                acc = ctx.add_cc(acc, ctx.rotate(group, (n - (s0 - b0)) % n))
             asm = asm + (ctx.counters - before)
             s0 = s1
         results.append(acc)

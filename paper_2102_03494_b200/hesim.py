@@ -248,6 +248,8 @@ class HeContext:
         self.debug_checks = debug_checks
         self.precondition_checks = precondition_checks
         self.last_noise_budget = None
+        # distinct rotation steps used (= Galois keys a real evaluation needs)
+        self.rotation_steps: set[int] = set()
         self._lib = lib
         self._levels = levels
         self._q_bits = q_bits
@@ -486,6 +488,7 @@ class HeContext:
             if not charge_identity:
                 self.elided_rotations += 1
             return ct
+        self.rotation_steps.add(k)
         if not ct.tracked:
             return SlotCiphertext(None, ct.depth, ct.params, ct.assembly_depth)
         return self._wrap(self.evaluator.rotate(ct.handle, k), ct.depth, ct.assembly_depth)
@@ -585,6 +588,7 @@ class HeContext:
             self.elided_rotations += len(cts)
             return cts
         self.counters.rot += len(cts)
+        self.rotation_steps.add(k)
         if not cts[0].tracked:
             return [SlotCiphertext(None, c.depth, c.params, c.assembly_depth) for c in cts]
         groups: dict[int, list[int]] = {}
@@ -635,6 +639,7 @@ class HeContext:
         live = [i for i, k in enumerate(ks) if k != 0]
         self.elided_rotations += len(cts) - len(live)
         self.counters.rot += len(live)
+        self.rotation_steps.update(ks[i] for i in live)
         if not live:
             return outs
         if not cts[live[0]].tracked:
@@ -666,6 +671,7 @@ class HeContext:
             elif not charge_identity:
                 self.elided_rotations += 1
         live = sorted({k for k in ks if k != 0})
+        self.rotation_steps.update(live)
         if not live:
             return outs
         if not ct.tracked:
@@ -706,6 +712,7 @@ class HeContext:
         (counted as such), fused on the device."""
         self.counters.rot += len(cts)
         self.counters.add_cc += len(cts)
+        self.rotation_steps.add(k)
         if not cts[0].tracked:
             return [SlotCiphertext(None, c.depth, c.params, c.assembly_depth) for c in cts]
         groups: dict[int, list[int]] = {}

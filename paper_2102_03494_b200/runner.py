@@ -239,6 +239,25 @@ def _logits(value, ctx):
     return out[0] if batch == 1 else out
 
 
+def _logits_layout(net: NetworkSpec, plan: PackingPlan) -> tuple[int, int]:
+    """(logit ciphertexts, payload slots per ciphertext) of a plan's final value,
+    from a count-only walk (no device work)."""
+    ctx = HeContext(net.scheme)
+    res = run_encrypted(net, plan, _zero_weights(net), None, ctx=ctx, track_values=False)
+    v = res.value
+    if isinstance(v, DensePacked):
+        return 1, v.occupied
+    return len(v.cts), v.rows
+
+
+def _zero_weights(net: NetworkSpec) -> WeightSet:
+    from .netspec import required_tensors, WeightTensor
+    ws = WeightSet()
+    for name, shape in required_tensors(net).items():
+        ws.add(WeightTensor(name, np.zeros(shape, dtype=np.int64), 8, 1.0))
+    return ws
+
+
 def _tensor(value, ctx):
     if isinstance(value, DensePacked):
         return dense_unpack(value, ctx)

@@ -9,6 +9,8 @@
   synthetic images in one ciphertext row pair, under 5-prime plaintext CRT.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -19,6 +21,7 @@ from paper_2102_03494_b200.runner import inference_params, run_encrypted, scheme
 from _shared import cfg0_network, load, network_from_fixture, reference_step_totals, replay, scheme_from, step_totals
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_reference_sequences_on_gpu(cuda_lib):
@@ -107,8 +110,8 @@ def test_h_im2col_moves_hoisted_on_gpu(cuda_lib, golden_lib):
     x = rng.integers(-5, 6, size=(2, 3, 5, 5))
     k = KernelSpec(d=2, stride=1, out_channels=1)
     words = []
+    sch = scheme_from(128, [65537], levels=4)          # one key seed for both libraries
     for lib in (cuda_lib, golden_lib):
-        sch = scheme_from(128, [65537], levels=4)
         ctx = HeContext(sch, batch=2, lib=lib)
         cols = h_im2col_from_dense(dense_pack(x, ctx), k, ctx)
         assert np.array_equal(conv_unpack(cols, ctx).astype(np.int64), plain_im2col(x, k))
@@ -132,3 +135,35 @@ def test_extra_networks_on_gpu(cuda_lib, golden_lib, idx):
     evg = gold.value.cts[0]._ctx.evaluator
     for a, b in zip(res.value.cts, gold.value.cts):
         assert np.array_equal(ev.read(a.handle), evg.read(b.handle))
+
+
+def test_cfg3_end_to_end_on_gpu(cuda_lib):
+    """BASELINE configs[3] (CIFAR-shaped, ring 2^16 on thread-block clusters, avg-pool,
+    ffconv-default plan) on one row pair: both images' logits equal the reference's
+    run_reference (tests/golden/cfg3.json), op counts and depths equal its report."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from bench import cfg3_setup
+    net, plan, ws, xs, rp, ref = cfg3_setup(2, seed=20210205)
+    ctx = HeContext(net.scheme, batch=2, lib=cuda_lib)
+    res = run_encrypted(net, plan, ws, xs, ctx=ctx)
+    assert [[int(v) for v in row] for row in res.logits] == ref
+    meta = load("cfg3.json")
+    assert step_totals(res.steps) == reference_step_totals(meta["count_rows"])
+    assert (res.depth, res.assembly_depth) == (meta["depth"], meta["assembly_depth"])
+    assert len(ctx.rotation_steps) < 200            # tree combine: ~log2 keys per combine (7,259 as a chain)
+
+
+@pytest.mark.parametrize("variant", range(8))
+def test_cfg4_variants_logits_on_gpu(cuda_lib, variant):
+    """BASELINE configs[4]: every rank/packing variant on one row pair decrypts to the
+    oracle's direct-loop logits, with the reference's rotation counts."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from bench import ABLATION, REF_ROTATIONS, _oracle_logits, ablation_setup
+    name, first = ABLATION[variant]
+    net, plan, ws, xs, rp = ablation_setup(first, 2, seed=20210205)
+    ctx = HeContext(net.scheme, batch=2, lib=cuda_lib)
+    res = run_encrypted(net, plan, ws, xs, ctx=ctx)
+    assert [[int(v) for v in row] for row in res.logits] == _oracle_logits(net, ws, xs)
+    assert res.counters.rot == REF_ROTATIONS[name]
