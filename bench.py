@@ -504,7 +504,10 @@ def run_cifar(args, rank, world, local_rank):
         t = torch.tensor([ms], device=f"cuda:{local_rank}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    got = [[int(v) for v in row] for row in np.asarray(logits).tolist()]
+    got = [[int(v) for v in row] for row in np.atleast_2d(np.asarray(logits)).tolist()]
+    # every image against the oracle's direct loops (the fixture images are also pinned
+    # to the reference's own run_reference logits, tests/golden/cfg3.json)
+    want = _oracle_logits(net, ws, xs) if os.environ.get("BENCH_CIFAR_ORACLE", "1") == "1" else None
     kb = ctypes.c_uint64()
     lib.call("fhe_ctx_key_bytes", ev.ctx, ctypes.byref(kb))
     rots = ctx.counters.rot - rot0
@@ -518,6 +521,9 @@ def run_cifar(args, rank, world, local_rank):
         # images with a fixture (the reference's run_reference logits): exact comparison
         "logits_checked": len(ref_logits),
         "logits_match_reference": got[:len(ref_logits)] == ref_logits if ref_logits else None,
+        "oracle_images_checked": len(want) if want is not None else 0,
+        "logits_match_oracle": got == want if want is not None else None,
+        "distinct_rotation_keys": len(ctx.rotation_steps),
         "logits_sample": [str(int(v)) for v in np.asarray(logits)[0][:3]],
         "kernel_ms": breakdown,
     }

@@ -97,10 +97,6 @@ int fhe_launch_count(fhe_ctx *ctx, uint64_t *out);
  * row (I)NTT, 2 l (l+1) n + 2 l n per key switch (inner product + ModDown
  * scaling), 2 l n per hoisted-dot term; elementwise ops are not counted. */
 int fhe_work_modmuls(fhe_ctx *ctx, double *out);
-/* development diagnostic: time `iters` launches of an n-point (inverse) NTT over
- * `rows` rows of modulus q_0 with a radix-2^W register core (W in {3,4,5,6});
- * *ms = average launch time, *mismatch = rows whose output differs from W = 4 */
-int fhe_bench_ntt(fhe_ctx *ctx, int W, int inverse, uint32_t rows, uint32_t iters, float *ms, uint32_t *mismatch);
 /* generate Galois keys for the given rotation steps now (otherwise lazily) */
 int fhe_keygen_rotations(fhe_ctx *ctx, const uint32_t *steps, uint32_t m);
 

@@ -524,10 +524,6 @@ int fhe_prof_enable(fhe_ctx *ctx, int on) { (void)ctx; (void)on; return 0; }
 int fhe_prof_report(fhe_ctx *ctx, char *buf, uint32_t len) { (void)ctx; if (len) buf[0] = 0; return 0; }
 int fhe_launch_count(fhe_ctx *ctx, uint64_t *out) { (void)ctx; *out = 0; return 0; }
 int fhe_work_modmuls(fhe_ctx *ctx, double *out) { (void)ctx; *out = 0.0; return 0; }
-int fhe_bench_ntt(fhe_ctx *ctx, int W, int inverse, uint32_t rows, uint32_t iters, float *ms, uint32_t *mismatch) {
-    (void)ctx; (void)W; (void)inverse; (void)rows; (void)iters; *ms = 0; *mismatch = 0;
-    return fail(FHE_EINVAL, "no device in the golden model");
-}
 int fhe_peak_modmul(fhe_ctx *ctx, uint32_t iters, double *out) {
     (void)ctx; (void)iters; *out = 0.0;
     return fail(FHE_EINVAL, "no device in the golden model");

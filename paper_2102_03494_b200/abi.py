@@ -60,8 +60,6 @@ SIGNATURES = {
     "fhe_prof_enable": (c_int, [c_void_p, c_int]),
     "fhe_prof_report": (c_int, [c_void_p, ctypes.c_char_p, c_uint32]),
     "fhe_launch_count": (c_int, [c_void_p, _U64P]),
-    "fhe_bench_ntt": (c_int, [c_void_p, c_int, c_int, c_uint32, c_uint32, POINTER(ctypes.c_float),
-                              POINTER(c_uint32)]),
     "fhe_ct_create": (c_int, [c_void_p, c_uint32, c_uint32, POINTER(c_void_p)]),
     "fhe_ct_destroy": (None, [c_void_p]),
     "fhe_ct_level": (c_uint32, [c_void_p]),

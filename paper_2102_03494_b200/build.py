@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib", "libffconv_he.so")
 SOURCES = ["ffconv_he.cu"]
-DEPS = ["ffconv_he.cu", "kernels.cuh", "ks_fused.cuh", "ntt_core.cuh", "ntt4.cuh", "arith.cuh"]
+DEPS = ["ffconv_he.cu", "kernels.cuh", "ks_fused.cuh", "ntt_core.cuh", "arith.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

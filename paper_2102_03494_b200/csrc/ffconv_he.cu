@@ -20,7 +20,6 @@
 #include "ffconv_he.h"
 #include "kernels.cuh"
 #include "ks_fused.cuh"
-#include "ntt4.cuh"
 
 // =================================================================== errors
 static thread_local char g_err[512];
@@ -771,100 +770,6 @@ extern "C" int fhe_prof_report(fhe_ctx *c, char *buf, uint32_t len) {
         buf[len - 1] = 0;
     }
     return 0;
-}
-
-template <int LOGN, int W>
-static int bench_variant(fhe_ctx *c, int inverse, u32 rows, u32 iters, const u64 *in, u64 *out, float *ms) {
-    using C = NttCfg<LOGN, W>;
-    const size_t smem = (size_t)C::SMEM_WORDS * 8;
-    auto kf = k_bench_fwd<LOGN, W>;
-    auto ki = k_bench_inv<LOGN, W>;
-    CU(cudaFuncSetAttribute((const void *)kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CU(cudaFuncSetAttribute((const void *)ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    for (u32 it = 0; it < iters + 2; it++) {
-        if (it == 2) cudaEventRecord(e0, c->st);
-        if (inverse) ki<<<rows, C::TH, smem, c->st>>>(in, out, c->d_mods, 0);
-        else kf<<<rows, C::TH, smem, c->st>>>(in, out, c->d_mods, 0);
-    }
-    cudaEventRecord(e1, c->st);
-    CU(cudaEventSynchronize(e1));
-    CHECK_LAUNCH();
-    cudaEventElapsedTime(ms, e0, e1);
-    *ms /= iters;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return 0;
-}
-
-template <int LOGN>
-static int bench_ntt4(fhe_ctx *c, int inverse, u32 rows, u32 iters, const u64 *in, u64 *out, float *ms) {
-    using C4 = Ntt4Cfg<LOGN>;
-    u64 *tmp;
-    CU(cudaMalloc((void **)&tmp, (size_t)rows * C4::N * 8));
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    const unsigned ga = rows * C4::CTAS_PER_ROW_A, gb = rows * C4::CTAS_PER_ROW_B;
-    for (u32 it = 0; it < iters + 2; it++) {
-        if (it == 2) cudaEventRecord(e0, c->st);
-        if (inverse) {
-            k4_inv_rows<LOGN><<<gb, C4::THB, 0, c->st>>>(in, tmp, c->d_mods, 0);
-            k4_inv_cols<LOGN><<<ga, C4::THA, 0, c->st>>>(tmp, out, c->d_mods, 0);
-        } else {
-            k4_fwd_cols<LOGN><<<ga, C4::THA, 0, c->st>>>(in, tmp, c->d_mods, 0);
-            k4_fwd_rows<LOGN><<<gb, C4::THB, 0, c->st>>>(tmp, out, c->d_mods, 0);
-        }
-    }
-    cudaEventRecord(e1, c->st);
-    CU(cudaEventSynchronize(e1));
-    CHECK_LAUNCH();
-    cudaEventElapsedTime(ms, e0, e1);
-    *ms /= iters;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaFree(tmp);
-    return 0;
-}
-
-extern "C" int fhe_bench_ntt(fhe_ctx *c, int W, int inverse, uint32_t rows, uint32_t iters, float *ms,
-                             uint32_t *mismatch) {
-    if (c->logn != 14) return fail(FHE_EINVAL, "bench_ntt is instantiated for n = 2^14 only");
-    size_t n = c->n;
-    u64 *in, *ref, *out;
-    CU(cudaMalloc((void **)&in, rows * n * 8));
-    CU(cudaMalloc((void **)&ref, rows * n * 8));
-    CU(cudaMalloc((void **)&out, rows * n * 8));
-    std::vector<u64> h(rows * n);
-    u64 q = c->P.q[0], x = 0x9E3779B97F4A7C15ull;
-    for (auto &v : h) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; v = x % q; }
-    CU(cudaMemcpy(in, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
-    float dummy;
-    int rc = bench_variant<14, 4>(c, inverse, rows, 1, in, ref, &dummy);
-    if (!rc) {
-        switch (W) {
-            case 4: rc = bench_variant<14, 4>(c, inverse, rows, iters, in, out, ms); break;
-            case 5: rc = bench_variant<14, 5>(c, inverse, rows, iters, in, out, ms); break;
-            case 6: rc = bench_variant<14, 6>(c, inverse, rows, iters, in, out, ms); break;
-            case 100: rc = bench_ntt4<14>(c, inverse, rows, iters, in, out, ms); break;
-            default: rc = fail(FHE_EINVAL, "W must be in {3,4,5,6}");
-        }
-    }
-    if (!rc) {
-        std::vector<u64> a(rows * n), b(rows * n);
-        cudaMemcpy(a.data(), ref, a.size() * 8, cudaMemcpyDeviceToHost);
-        cudaMemcpy(b.data(), out, b.size() * 8, cudaMemcpyDeviceToHost);
-        u32 bad = 0;
-        for (u32 r = 0; r < rows; r++)
-            if (memcmp(a.data() + r * n, b.data() + r * n, n * 8)) bad++;
-        *mismatch = bad;
-    }
-    cudaFree(in);
-    cudaFree(ref);
-    cudaFree(out);
-    return rc;
 }
 
 extern "C" int fhe_work_modmuls(fhe_ctx *c, double *out) {

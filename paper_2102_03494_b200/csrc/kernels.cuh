@@ -1002,41 +1002,6 @@ __global__ void k_peak_modmul(u64 *sink, u32 iters, u64 q, u64 w, u64 wsh) {
     if (acc == 0x1234567ull) sink[0] = acc;
 }
 
-// ---------------------------------------------------------------- diagnostics
-// NTT core variants for the development benchmark (fhe_bench_ntt): one row per
-// CTA, coalesced load, core, coalesced store.
-template <int LOGN, int W>
-__global__ void __launch_bounds__(NttCfg<LOGN, W>::TH) k_bench_fwd(const u64 *in, u64 *out, const ModInfo *mods, int mid) {
-    using C = NttCfg<LOGN, W>;
-    extern __shared__ u64 sm[];
-    const int tid = threadIdx.x;
-    const ModInfo M = mods[mid];
-    const u64 *src = in + (long long)blockIdx.x * C::N;
-    u64 v[C::E];
-#pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = src[(e << (LOGN - C::W)) | tid];
-    ntt_fwd_core<LOGN, W>(v, sm, M, tid);
-    u64 *dst = out + (long long)blockIdx.x * C::N;
-    for (int i = tid; i < C::N; i += C::TH) dst[i] = sm[C::pad(i)];
-}
-
-template <int LOGN, int W>
-__global__ void __launch_bounds__(NttCfg<LOGN, W>::TH) k_bench_inv(const u64 *in, u64 *out, const ModInfo *mods, int mid) {
-    using C = NttCfg<LOGN, W>;
-    extern __shared__ u64 sm[];
-    const int tid = threadIdx.x;
-    const ModInfo M = mods[mid];
-    const u64 *src = in + (long long)blockIdx.x * C::N;
-    #pragma unroll
-    for (int i = tid, e_ = 0; e_ < C::E; i += C::TH, e_++) sm[C::pad(i)] = src[i];
-    __syncthreads();
-    u64 v[C::E];
-    ntt_inv_core<LOGN, W>(v, sm, M, tid);
-    u64 *dst = out + (long long)blockIdx.x * C::N;
-#pragma unroll
-    for (int e = 0; e < C::E; e++) dst[(e << (LOGN - C::W)) | tid] = v[e];
-}
-
 // ------------------------------------------------------------ hoisted dot
 // out[s][c][i][j] = sum_k R[k][c][i][j] * tau_{g_k}(pt[s])[t][i][j]   (c = (t, r, poly))
 // CTA = 32 coefficients x 8 outputs (one warp per output); R tiles of 8 rotations x
