@@ -466,12 +466,19 @@ def run_cifar(args, rank, world, local_rank):
     lo, hi = shard_range(args.images, rank, world)
     per_rank = hi - lo
     net, plan, ws, xs, rp, ref_logits = cfg3_setup(per_rank, seed=CFG1["seed"], offset=lo)
-    ctx = HeContext(net.scheme, batch=per_rank, lib=lib, schedule=args.schedule)
+    ctx = HeContext(net.scheme, batch=min(args.chunk, per_rank), lib=lib, schedule=args.schedule,
+                    level_schedule=args.level_schedule)
     ev = ctx.evaluator
     stream_ptr = ctypes.c_void_p()
     lib.call("fhe_ctx_stream", ev.ctx, ctypes.byref(stream_ptr))
     stream = torch.cuda.ExternalStream(stream_ptr.value, device=local_rank)
-    packed = pack_input(net, plan, xs, ctx)
+    chunk = ctx.batch
+    parts = []
+    for i in range(0, per_rank, chunk):
+        sub = xs[i:i + chunk]
+        if len(sub) < chunk:                                   # ragged tail: zero images
+            sub = np.concatenate([sub, np.zeros((chunk - len(sub),) + sub.shape[1:], dtype=sub.dtype)])
+        parts.append(pack_input(net, plan, sub, ctx))
     ev.sync()
     if world > 1:
         torch.distributed.barrier()
@@ -483,12 +490,15 @@ def run_cifar(args, rank, world, local_rank):
     if prof:
         lib.call("fhe_prof_enable", ev.ctx, 1)
     t0 = time.perf_counter()
+    results = []
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
         e0.record(stream)
-        res = run_encrypted(net, plan, ws, None, ctx=ctx, packed=packed, decrypt=False)
+        for packed in parts:
+            results.append(run_encrypted(net, plan, ws, None, ctx=ctx, packed=packed, decrypt=False))
         e1.record(stream)
         e1.synchronize()
+    res = results[-1]
     ms = e0.elapsed_time(e1)
     wall = time.perf_counter() - t0
     breakdown = None
@@ -499,7 +509,7 @@ def run_cifar(args, rank, world, local_rank):
         breakdown = {k: {"calls": c, "ms": round(m, 3)} for k, (c, m) in parse_prof(buf.value.decode()).items()}
     cnt1 = ctypes.c_uint64()
     lib.call("fhe_launch_count", ev.ctx, ctypes.byref(cnt1))
-    logits = _decrypt_logits(res, ctx)
+    logits = np.concatenate([np.atleast_2d(_decrypt_logits(r, ctx)) for r in results])[:per_rank]
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{local_rank}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -584,7 +594,7 @@ def run_ablation(args, rank, world, local_rank):
     for name, first in ABLATION:
         net, plan, ws, xs, rp = ablation_setup(first, per_rank, seed=CFG1["seed"], offset=lo)
         chunk = min(args.chunk, per_rank)
-        ctx = HeContext(net.scheme, batch=chunk, lib=lib)
+        ctx = HeContext(net.scheme, batch=chunk, lib=lib, level_schedule=args.level_schedule)
         chunks = [xs[i:i + chunk] for i in range(0, per_rank, chunk)]
         if len(chunks[-1]) < chunk:
             pad = np.zeros((chunk - len(chunks[-1]),) + xs.shape[1:], dtype=xs.dtype)
@@ -654,7 +664,7 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     rounds = -(-per_rank // chunk)
     net, plan, ws, xs_all, rp = cfg0_setup(images_total, seed=CFG1["seed"])
     schedule = schedule or args.schedule
-    ctx = HeContext(net.scheme, batch=chunk, lib=lib, schedule=schedule)
+    ctx = HeContext(net.scheme, batch=chunk, lib=lib, schedule=schedule, level_schedule=args.level_schedule)
     ev = ctx.evaluator
     stream_ptr = ctypes.c_void_p()
     lib.call("fhe_ctx_stream", ev.ctx, ctypes.byref(stream_ptr))
@@ -767,7 +777,7 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     in_bytes = rounds * world * in_cts * rp.T * ctx.rows * rp.n * 8
     out_bytes = rounds * world * n_logit_cts * rp.T * ctx.rows * 2 * m_logit * 8
     return {
-        "schedule": schedule,
+        "schedule": schedule, "level_schedule": bool(args.level_schedule),
         "images_per_s": images_total * steps / (ms * 1e-3),
         "ms_per_step": ms / steps,
         "e2e_images_per_s": images_total / e2e_s,
@@ -921,6 +931,8 @@ def main():
     ap.add_argument("--no-inference", action="store_true", help="rotation workload: skip the inference sample")
     ap.add_argument("--schedule", choices=["reference", "hoisted"], default="reference",
                     help="inference: rotate-and-sum schedule (hoisted = top levels as a ct x pt GEMM)")
+    ap.add_argument("--no-level-schedule", dest="level_schedule", action="store_false",
+                    help="inference: keep every ciphertext at the top level (no modulus switching between steps)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

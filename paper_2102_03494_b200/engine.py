@@ -175,14 +175,39 @@ def _hoisted(ctx) -> bool:
     return getattr(ctx, "schedule", "reference") == "hoisted" and hasattr(ctx, "hoisted_dot")
 
 
+def level_down(ctx, cts, extra_bits: float):
+    """Level schedule inside a plan step (HeContext(level_schedule=True)): the runner
+    records the model's noise consumption before the step (ctx.noise_consumed); once
+    the step's own operations so far (`extra_bits`) let the budget absorb dropping
+    q primes, the ciphertexts are modulus-switched before the rotation-heavy part."""
+    if not getattr(ctx, "level_schedule", False) or getattr(ctx, "noise_consumed", None) is None:
+        return cts
+    cts = list(cts)
+    if not cts or not cts[0].tracked:
+        return cts
+    from .runner import _target_level
+    ev = ctx.evaluator
+    target = _target_level(ev.params.q, ev.L, ctx.noise_consumed + extra_bits)
+    out = []
+    for c in cts:
+        while c.handle.level > target:
+            c = ctx.mod_switch(c)
+        out.append(c)
+    return out
+
+
+def _t_bits(ctx) -> float:
+    import math
+    return math.log2(max(ctx.params.factors())) if hasattr(ctx.params, "factors") else 0.0
+
+
 def _products_and_sums(ctx, ct, pvs, m: int, hoist):
     """rotate_and_sum(ct * pv, m) for every pv.  Reference schedule: one product
     and ceil(log2 m) rotate-add levels each.  Hoisted schedule: the top h levels of
     every tree as one ct x pt GEMM over the shared input's rotations."""
-    if hoist is None:
-        return _rotate_and_sum_many(ctx, _mul_plain_many(ctx, [ct] * len(pvs), pvs), m)
-    if hoist.h == 0:
-        return _rotate_and_sum_many(ctx, _mul_plain_many(ctx, [ct] * len(pvs), pvs), m)
+    if hoist is None or hoist.h == 0:
+        prods = level_down(ctx, _mul_plain_many(ctx, [ct] * len(pvs), pvs), _t_bits(ctx) + 8)
+        return _rotate_and_sum_many(ctx, prods, m)
     outs = ctx.hoisted_dot(hoist.rotated, hoist.ks, pvs)
     for step in hoist.tail:
         outs = ctx._rotate_add_many(outs, step)
@@ -220,7 +245,7 @@ def _dense_assemble(x, w, kernel, ctx, blocks):
             outs = _dense_dots(x, w, kernel, ctx, o, s0 - o * rows, s1 - o * rows, hoist)
             dots = dots + (ctx.counters - before)
             before = ctx.counters.copy()
-            masked = _mask_slot0_many(ctx, outs)
+            masked = level_down(ctx, _mask_slot0_many(ctx, outs), 2 * _t_bits(ctx) + 17)   # dot + mask
             # the group's outputs as one contiguous block (tree: log2 keys), then placed
             # at its offset in the block: len - 1 + 1 rotations, as the chain's
             group, _ = tree_combine(ctx, masked, [1] * len(masked))
@@ -335,7 +360,7 @@ def fc_dense(x: DensePacked, w: WeightMatrix, bias: BiasVector | None, ctx, mask
         rows = rows + (ctx.counters - before)
         if mask_outputs:
             before = ctx.counters.copy()
-            red = _mask_slot0_many(ctx, red)
+            red = level_down(ctx, _mask_slot0_many(ctx, red), 2 * _t_bits(ctx) + 17)
             masks = masks + (ctx.counters - before)
         outs.extend(red)
     phases = [PhaseCost("row-products", rows)]

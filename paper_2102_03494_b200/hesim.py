@@ -237,7 +237,8 @@ class HeContext:
 
     def __init__(self, params: SchemeParams, *, batch: int = 1, lib=None, levels: int | None = None,
                  q_bits: int | None = None, debug_checks: bool = False, pt_cache: bool = True,
-                 schedule: str = "reference", hoist_levels: int = 7, precondition_checks: bool = True):
+                 schedule: str = "reference", hoist_levels: int = 7, precondition_checks: bool = True,
+                 level_schedule: bool = False):
         if batch < 1:
             raise ValueError("batch must be >= 1")
         self.params = params
@@ -247,6 +248,10 @@ class HeContext:
         self.rows = (batch + 1) // 2
         self.debug_checks = debug_checks
         self.precondition_checks = precondition_checks
+        # runner.run_encrypted drops q primes between plan steps once the noise model says
+        # the budget allows it (runner._target_level): same slots, cheaper key switches
+        self.level_schedule = level_schedule
+        self.noise_consumed = None
         self.last_noise_budget = None
         # distinct rotation steps used (= Galois keys a real evaluation needs)
         self.rotation_steps: set[int] = set()

@@ -117,37 +117,64 @@ def static_bounds(net: NetworkSpec, ws: WeightSet, input_bound: int) -> list[int
 # at t = 30 bits the cfg0 chain measured fresh 35, dot+rotate-and-sum 43, slot
 # mask 32, assembly chain 6, 1x1 scalar stage 4, combine 2-6, square 41 bits.
 # Each term below is the measurement + 1 bit; 12 bits of margin on top.
-def _noise_bits(plan: PackingPlan, t_bits: float, mask_fc: bool, plain_conv_conv: bool = False) -> float:
-    """plain_conv_conv: the column stage multiplies by a masked constant plaintext
+def _step_noise_bits(plan: PackingPlan, k: int, t_bits: float, mask_fc: bool, plain_conv_conv: bool = False) -> float:
+    """Invariant-noise bits plan step k adds (the per-op costs above).
+    plain_conv_conv: the column stage multiplies by a masked constant plaintext
     (the reference engine, engine.py:189-195) instead of a scalar (engine.conv_conv
     here): about a slot mask's noise per stage instead of a few bits."""
     dot, mask, chain, square = t_bits + 14, t_bits + 3, 7, t_bits + 12
     cols = mask + 4 if plain_conv_conv else 5
-    need = t_bits + 6                                 # fresh encryption
-    for k, step in enumerate(plan.steps):
-        op = step.op
-        if op == CONV_DENSE or (op == FFCONV and step.pattern in ("DP-HI2C-CP", "DP-DP")):
+    step = plan.steps[k]
+    op, need = step.op, 0.0
+    if op == CONV_DENSE or (op == FFCONV and step.pattern in ("DP-HI2C-CP", "DP-DP")):
+        need += dot + mask + chain
+    if op == FFCONV:
+        need += cols                                  # 1x1 stage
+        if step.pattern in ("CP-HI2C-CP", "CP-HI2C-DP"):
+            need += cols
+        if step.pattern == "DP-DP":
             need += dot + mask + chain
-        if op == FFCONV:
-            need += cols                                  # 1x1 stage
-            if step.pattern in ("CP-HI2C-CP", "CP-HI2C-DP"):
-                need += cols
-            if step.pattern == "DP-DP":
-                need += dot + mask + chain
-        if op == CONV_COLUMNS:
-            need += cols + 3
-        if op in (HIM2COL_DENSE, HIM2COL_CONV, GROUP_DENSE):
-            need += mask + chain
-        if op == SQUARE:
-            need += square
-        if op == FC:
-            need += dot
-            nxt = plan.steps[k + 1].op if k + 1 < len(plan.steps) else None
-            if mask_fc and nxt == COMBINE:
-                need += mask
-        if op == COMBINE:
-            need += chain
+    if op == CONV_COLUMNS:
+        need += cols + 3
+    if op in (HIM2COL_DENSE, HIM2COL_CONV, GROUP_DENSE):
+        need += mask + chain
+    if op == SQUARE:
+        need += square
+    if op == FC:
+        need += dot
+        nxt = plan.steps[k + 1].op if k + 1 < len(plan.steps) else None
+        if mask_fc and nxt == COMBINE:
+            need += mask
+    if op == COMBINE:
+        need += chain
+    return need
+
+
+def _noise_bits(plan: PackingPlan, t_bits: float, mask_fc: bool, plain_conv_conv: bool = False) -> float:
+    """Bits of q the whole plan needs: fresh encryption + every step + 12 bits of margin."""
+    need = t_bits + 6                                 # fresh encryption
+    for k in range(len(plan.steps)):
+        need += _step_noise_bits(plan, k, t_bits, mask_fc, plain_conv_conv)
     return need + 12.0
+
+
+# Level schedule (HeContext(level_schedule=True)).  BFV modulus switching keeps the noise
+# budget: switching Q -> Q/q_last divides the noise by q_last and adds a rounding term of
+# about the fresh-encryption noise.  So once the plan's steps have added more than
+# log2(q_last) + SLACK bits of noise since encryption, the last prime can be dropped
+# for free, and every later key switch runs at fewer primes (its cost grows as l^2).
+LEVEL_SLACK_BITS = 12.0
+
+
+def _target_level(q: tuple, level: int, consumed: float) -> int:
+    """The lowest level reachable by dropping primes from `level` whose bits sum to at
+    most consumed - LEVEL_SLACK_BITS (never below 2)."""
+    room = consumed - LEVEL_SLACK_BITS
+    drop = 0
+    while level - drop > 2 and room >= math.log2(q[level - drop - 1]):
+        room -= math.log2(q[level - drop - 1])
+        drop += 1
+    return level - drop
 
 
 def inference_params(net: NetworkSpec, plan: PackingPlan, ws: WeightSet, input_bound: int, *,
@@ -303,7 +330,13 @@ def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input
             raise ValueError(f"input shape {x_in.shape} does not match (c, h, w) = {shape}")
     records, layer_depths, layer_outputs = [], [], []
     value = None
+    sched = bool(getattr(ctx, "level_schedule", False)) and track_values
+    if sched:
+        t_bits = math.log2(max(ctx.params.factors()))
+        qs, top, consumed = ctx.evaluator.params.q, ctx.evaluator.L, 0.0
     for k, step in enumerate(plan.steps):
+        if sched:
+            ctx.noise_consumed = consumed            # the engine's in-step level_down reads it
         before = ctx.counters.copy()
         d_before = packed_depth(value) if value is not None else (0, 0)
         phases = None
@@ -345,6 +378,9 @@ def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input
             value, phases = _run_ffconv(step, value, weights, ctx)
         else:
             raise ValueError(f"cannot execute step {op!r}")
+        if sched and op not in (PACK_DENSE, PACK_COLUMNS):
+            consumed += _step_noise_bits(plan, k, t_bits, mask_fc)
+            value = _switch_value(value, ctx, _target_level(qs, top, consumed))
         if phases is None:
             phases = [("total", ctx.counters - before)]
         else:
@@ -357,10 +393,29 @@ def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input
                                  "assembly_delta": d_after[1] - d_before[1]})
             if capture_layers and track_values:
                 layer_outputs.append((step.layer_index, _tensor(value, ctx)))
+    if sched:
+        ctx.noise_consumed = None
     logits = _logits(value, ctx) if (track_values and decrypt) else None
     depth, adepth = packed_depth(value)
     return RunResult(logits, records, ctx.counters.copy(), depth, adepth, layer_depths, layer_outputs,
                      ctx.elided_rotations, value)
+
+
+def _switch_value(value, ctx, level: int):
+    """Modulus-switch every ciphertext of a packed value down to `level` (uncounted,
+    as in hesim.HeContext.mod_switch)."""
+    def down(ct):
+        while ct.tracked and ct.handle.level > level:
+            ct = ctx.mod_switch(ct)
+        return ct
+    if isinstance(value, DensePacked):
+        return DensePacked(down(value.ct), value.shape)
+    if isinstance(value, ChannelPacked):
+        return ChannelPacked(tuple(down(c) for c in value.cts), value.spatial)
+    from .packing import ConvPacked
+    if isinstance(value, ConvPacked):
+        return ConvPacked(tuple(down(c) for c in value.cts), value.spatial)
+    return value
 
 
 def _run_ffconv(step, value, ws, ctx):

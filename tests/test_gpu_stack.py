@@ -167,3 +167,24 @@ def test_cfg4_variants_logits_on_gpu(cuda_lib, variant):
     res = run_encrypted(net, plan, ws, xs, ctx=ctx)
     assert [[int(v) for v in row] for row in res.logits] == _oracle_logits(net, ws, xs)
     assert res.counters.rot == REF_ROTATIONS[name]
+
+
+@pytest.mark.parametrize("schedule", ["reference", "hoisted"])
+def test_cfg0_level_schedule_on_gpu(cuda_lib, schedule):
+    """Level schedule (HeContext(level_schedule=True)): q primes are dropped between and
+    inside plan steps once the noise model allows; the logits stay the reference's, the
+    op counts are unchanged and the budget is not exhausted."""
+    from paper_2102_03494_b200.hesim import SchemeParams
+    net0, ws, xs, meta = cfg0_network(SchemeParams(n_slots=8192, t=(1 << 61) - 1))
+    rp = inference_params(net0, build_plan(net0, "explicit"), ws, input_bound=255)
+    net, _, _, _ = cfg0_network(scheme_for(rp))
+    plan = build_plan(net, "explicit")
+    ctx = HeContext(net.scheme, batch=2, lib=cuda_lib, schedule=schedule, level_schedule=True)
+    res = run_encrypted(net, plan, ws, xs, ctx=ctx)
+    for row, want in zip(res.logits, meta["logits"]):
+        assert [str(int(v)) for v in row] == want
+    assert max(ct.handle.level for ct in res.value.cts) < rp.L
+    assert ctx.last_noise_budget > 3
+    if schedule == "reference":
+        c = res.counters
+        assert (c.mul_pc, c.add_cc, c.rot, c.mul_cc, c.assembly_mul_pc) == (458, 4894, 4889, 2, 438)
