@@ -799,6 +799,40 @@ def run_inference(args, rank, world, local_rank, images_total=None, steps=None, 
     }
 
 
+def run_latency(args, local_rank, schedule="reference"):
+    """configs[0]: one synthetic image, end to end on one GPU -- host pixels -> encrypt ->
+    evaluate -> decrypt -> host logits -- and the device time of the evaluation alone
+    (CUDA events); a warm-up run first builds keys and plaintexts."""
+    import torch
+    from paper_2102_03494_b200.abi import cuda_library
+    from paper_2102_03494_b200.hesim import HeContext
+    from paper_2102_03494_b200.runner import pack_input, run_encrypted
+    torch.cuda.set_device(local_rank)
+    lib = cuda_library()
+    net, plan, ws, xs, rp = cfg0_setup(1, seed=CFG1["seed"])
+    ctx = HeContext(net.scheme, batch=1, lib=lib, schedule=schedule, level_schedule=args.level_schedule)
+    ev = ctx.evaluator
+    stream_ptr = ctypes.c_void_p()
+    lib.call("fhe_ctx_stream", ev.ctx, ctypes.byref(stream_ptr))
+    stream = torch.cuda.ExternalStream(stream_ptr.value, device=local_rank)
+    run_encrypted(net, plan, ws, xs[0], ctx=ctx)                    # warm-up: keys, plaintexts
+    packed = pack_input(net, plan, xs[0], ctx)
+    ev.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run_encrypted(net, plan, ws, None, ctx=ctx, packed=packed, decrypt=False)
+    e1.record(stream)
+    e1.synchronize()
+    dev_ms = e0.elapsed_time(e1)
+    t0 = time.perf_counter()
+    res = run_encrypted(net, plan, ws, xs[0], ctx=ctx)
+    e2e_ms = 1e3 * (time.perf_counter() - t0)
+    ok = [int(v) for v in res.logits] == _oracle_logits(net, ws, xs)[0]
+    return {"workload": "configs[0]: one 28x28 image (zero-padded to 29x29), batch 1", "schedule": schedule,
+            "level_schedule": bool(args.level_schedule), "device_ms": dev_ms, "e2e_ms": e2e_ms,
+            "logits_match": ok, "crt_primes": rp.T, "L": rp.L}
+
+
 def _oracle_logits(net, ws, xs):
     """Reference logits of every image (object ints) from the oracle's direct loops."""
     from oracle.slot_oracle import run_reference_ints
@@ -925,7 +959,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["rotation", "inference", "ablation", "cifar"], default="rotation")
+    ap.add_argument("--workload", choices=["rotation", "inference", "ablation", "cifar", "latency"], default="rotation")
     ap.add_argument("--images", type=int, default=256, help="inference: images per step (whole job)")
     ap.add_argument("--chunk", type=int, default=64, help="inference: images per ciphertext batch")
     ap.add_argument("--no-inference", action="store_true", help="rotation workload: skip the inference sample")
@@ -978,6 +1012,13 @@ def main():
             import torch
             torch.distributed.destroy_process_group()
         return
+    if args.workload == "latency":
+        if rank == 0:
+            lat = {s: run_latency(args, local_rank, schedule=s) for s in ("reference", "hoisted")}
+            print(json.dumps({"metric": "configs[0] single-image latency (ms, end to end)",
+                              "value": lat["reference"]["e2e_ms"], "unit": "ms", "n_gpus": 1,
+                              "higher_is_better": False, "latency": lat}), flush=True)
+        return
     if args.workload == "inference":
         inf = run_inference(args, rank, world, local_rank)
         res = {
@@ -1011,6 +1052,8 @@ def main():
                                                          "logical_rotations_per_chunk", "roofline",
                                                          "kernel_ms_one_chunk", "logits_check")}
         res["rates"]["images_per_s_hoisted"] = hinf["images_per_s"]
+        if world == 1:
+            res["latency_cfg0"] = run_latency(args, local_rank)
     if rank == 0 and world == 1:
         rate, sample = cpu_baseline_rotation(1, seconds=3.0)
         res["cpu_baseline"] = {"value": rate, "unit": "rotations/s", "cores": 1, "kind": "port",

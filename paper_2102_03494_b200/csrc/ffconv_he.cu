@@ -551,6 +551,7 @@ static int setup_workspace(fhe_ctx *c) {
     if (!env && S < 8) S = 8;          // large rings: keep >= 8 ciphertexts per sub-batch
     if (S < 1) S = 1;
     if (S > MAXS) S = MAXS;
+    if (!env && S > 64) S = 64;        // default sub-batch (FHE_KS_BATCH up to MAXS)
     c->S = S;
     const char *lenv = getenv("FHE_LANES");
     c->lanes = lenv ? std::max(1, std::min(fhe_ctx::MAXLANES, atoi(lenv))) : 2;
@@ -1248,10 +1249,9 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     // inner-product variant: (ciphertexts per thread, min CTAs per SM); env FHE_KS_VARIANT=0..3
     static int ksv = -1;
     if (ksv < 0) { const char *e = getenv("FHE_KS_VARIANT"); ksv = e ? atoi(e) : 2; }   // 2: measured best (4 cts/thread, 4 CTAs/SM)
-    const int G = (ksv == 1 || ksv == 3 || ksv == 5) ? 2 : 4;
-    const bool vec2 = ksv >= 4 && n >= 4;     // 4, 5: two coefficients per thread (16-byte accesses)
+    const int G = (ksv == 1 || ksv == 3) ? 2 : 4;
     c->alg_mm += (double)S * (2.0 * l * (l + 1) + 2.0 * l) * n;   // key inner product + ModDown scaling
-    long long tot = (long long)((S + G - 1) / G) * l * (vec2 ? n / 2 : n);
+    long long tot = (long long)((S + G - 1) / G) * l * n;
     // fold the addends into the inner product while its Montgomery input bound holds
     // ((l + 2) q_i < 2^64: l digit terms + 2 addend terms, each < q_i^2); else the
     // rescale epilogue adds them
@@ -1278,14 +1278,10 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
         const unsigned nb = (unsigned)nblocks(tot);
 #define KS_LAUNCH(LLV, GV, MB) k_ks_inner<LLV, GV, MB><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, \
                                                         (int)c->logn, c->special_id, c->d_mods, kad)
-#define KS_LAUNCH2(LLV, GV, MB) k_ks_inner2<LLV, GV, MB><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, \
-                                                        (int)c->logn, c->special_id, c->d_mods, kad)
 #define KS_CASE(LLV) case LLV:                                        \
         if (ksv == 1) KS_LAUNCH(LLV, 2, 1);                           \
         else if (ksv == 2) KS_LAUNCH(LLV, 4, 4);                      \
         else if (ksv == 3) KS_LAUNCH(LLV, 2, 4);                      \
-        else if (ksv == 4) KS_LAUNCH2(LLV, 4, 2);                     \
-        else if (ksv == 5) KS_LAUNCH2(LLV, 2, 2);                     \
         else KS_LAUNCH(LLV, 4, 1);                                    \
         break;
         switch (l) {
@@ -1296,7 +1292,6 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
         }
 #undef KS_CASE
 #undef KS_LAUNCH
-#undef KS_LAUNCH2
     }
     CHECK_LAUNCH();
     // the special prime's inner product + ModDown INTT of both accumulators (one row each)

@@ -11,7 +11,7 @@
 #define MAXQ 24
 #define MAXB 26
 #define MAXT 8
-#define MAXS 64   // physical ciphertexts per key-switching sub-batch
+#define MAXS 128  // physical ciphertexts per key-switching sub-batch (kernel parameter tables)
 
 struct LevelDev {
     // decryption / encryption (per plaintext modulus k)
@@ -486,95 +486,6 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
             u64 *ob = Acc + ((u32)s * 2 * (l + 1) + i) * n + x;
             ob[0] = mont_reduce(h0, l0, q, qi);
             ob[estride] = mont_reduce(h1, l1, q, qi);
-        }
-    }
-}
-
-// The same inner product with two adjacent coefficients per thread: every row access
-// is a 16-byte load or store (twice the bytes in flight per load instruction; the
-// kernel is bound by memory latency).  Reads through an
-// automorphism (hoisted Ext, the diagonal, the c0 addend) stay 8-byte gathers.
-DEV void mac128x2(u64 (&h)[2], u64 (&lo)[2], const ulonglong2 &a, const ulonglong2 &b) {
-    mac128(h[0], lo[0], a.x, b.x);
-    mac128(h[1], lo[1], a.y, b.y);
-}
-template <int LL, int KS_GROUP, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_ks_inner2(const u64 *__restrict__ Ext, DigitTab dt, u64 *__restrict__ Acc,
-                                                      int S, int L, int logn, int special_id,
-                                                      const ModInfo *__restrict__ mods, const KsAdd ka_) {
-    constexpr int l = LL;
-    const u32 n = 1u << logn, nh = n >> 1;
-    const u32 groups = (S + KS_GROUP - 1) / KS_GROUP;
-    const u32 total = groups * l * nh;
-    const u32 estride = (l + 1) * n;
-    const u32 kstride = 2u * (L + 1) * n;
-    for (u32 idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-        const u32 x = 2 * (idx & (nh - 1));
-        const u32 r = idx >> (logn - 1);
-        const int i = (int)(r % l);
-        const int s0 = KS_GROUP * (int)(r / l);
-        const ModInfo &M = mods[i];
-        const u64 q = M.q, qi = M.qinv;
-        const u32 kb0 = (u32)i * n + x, ka0 = (u32)(L + 1 + i) * n + x;
-        ulonglong2 kb[l], kav[l];
-        const int sc = S - s0 < KS_GROUP ? S - s0 : KS_GROUP;
-        const u64 *cur = dt.key[s0];
-#pragma unroll
-        for (int j = 0; j < l; j++) {
-            kb[j] = __ldg(reinterpret_cast<const ulonglong2 *>(cur + j * kstride + kb0));
-            kav[j] = __ldg(reinterpret_cast<const ulonglong2 *>(cur + j * kstride + ka0));
-        }
-        for (int u = 0; u < sc; u++) {
-            const int s = s0 + u;
-            if (dt.key[s] != cur) {
-                cur = dt.key[s];
-#pragma unroll
-                for (int j = 0; j < l; j++) {
-                    kb[j] = __ldg(reinterpret_cast<const ulonglong2 *>(cur + j * kstride + kb0));
-                    kav[j] = __ldg(reinterpret_cast<const ulonglong2 *>(cur + j * kstride + ka0));
-                }
-            }
-            const u32 pg = dt.perm[s], dg = dt.dperm[s];
-            const u32 es = pg ? dt.esrc[s] : (u32)s;
-            const u64 *eb = Ext + (es * l * (l + 1) + i) * n;
-            const u64 *db = dt.ntt[s] + (u32)i * n;
-            ulonglong2 e[l];
-#pragma unroll
-            for (int j = 0; j < l; j++) {
-                if (i == j) e[j] = dg ? make_ulonglong2(db[galois_perm(x, dg, logn)], db[galois_perm(x + 1, dg, logn)])
-                                      : *reinterpret_cast<const ulonglong2 *>(db + x);
-                else e[j] = pg ? make_ulonglong2(eb[j * estride + galois_perm(x, pg, logn)],
-                                                 eb[j * estride + galois_perm(x + 1, pg, logn)])
-                               : *reinterpret_cast<const ulonglong2 *>(eb + j * estride + x);
-            }
-            u64 h0[2] = {0, 0}, l0[2] = {0, 0}, h1[2] = {0, 0}, l1[2] = {0, 0};
-#pragma unroll
-            for (int j = 0; j < l; j++) {
-                mac128x2(h0, l0, e[j], kb[j]);
-                mac128x2(h1, l1, e[j], kav[j]);
-            }
-            {
-                const u64 pr = ka_.pr[i];
-                const ulonglong2 prv = make_ulonglong2(pr, pr);
-                if (const u64 *ad = ka_.add[s]) {
-                    const u32 ag = ka_.add_g[s];
-                    const u64 *a0 = ad + (u32)i * n, *a1 = ad + ka_.add_pstride + (u32)i * n;
-                    if (ka_.add_pmask & 1)
-                        mac128x2(h0, l0, ag ? make_ulonglong2(a0[galois_perm(x, ag, logn)], a0[galois_perm(x + 1, ag, logn)])
-                                            : *reinterpret_cast<const ulonglong2 *>(a0 + x), prv);
-                    if (ka_.add_pmask & 2)
-                        mac128x2(h1, l1, ag ? make_ulonglong2(a1[galois_perm(x, ag, logn)], a1[galois_perm(x + 1, ag, logn)])
-                                            : *reinterpret_cast<const ulonglong2 *>(a1 + x), prv);
-                }
-                if (const u64 *ac = ka_.acc[s]) {
-                    mac128x2(h0, l0, *reinterpret_cast<const ulonglong2 *>(ac + (u32)i * n + x), prv);
-                    mac128x2(h1, l1, *reinterpret_cast<const ulonglong2 *>(ac + ka_.acc_pstride + (u32)i * n + x), prv);
-                }
-            }
-            u64 *ob = Acc + ((u32)s * 2 * (l + 1) + i) * n + x;
-            *reinterpret_cast<ulonglong2 *>(ob) = make_ulonglong2(mont_reduce(h0[0], l0[0], q, qi), mont_reduce(h0[1], l0[1], q, qi));
-            *reinterpret_cast<ulonglong2 *>(ob + estride) =
-                make_ulonglong2(mont_reduce(h1[0], l1[0], q, qi), mont_reduce(h1[1], l1[1], q, qi));
         }
     }
 }
