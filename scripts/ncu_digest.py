@@ -1,0 +1,57 @@
+"""Digest an ncu report into small text (run next to the report; the .ncu-rep files are
+tens of MB and do not fit gpurun's return budget).
+
+    python scripts/ncu_digest.py <rep.ncu-rep> <out.txt> [top_n]
+
+Writes the details page (speed of light, occupancy, warp-state and pipe metrics) and the
+top SASS instructions by warp-stall samples with their opcode mix totals.
+"""
+import collections
+import csv
+import subprocess
+import sys
+
+
+def main(rep, out, top=60):
+    det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(src.splitlines()))
+    hdr = None
+    data = []
+    for r in rows:
+        if len(r) > 3 and r[0] == "Address":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    stall_key = "Warp Stall Sampling (All Samples)"
+    for d in data:
+        try:
+            d["_s"] = int(d.get(stall_key, "0") or 0)
+            d["_e"] = int(d.get("Instructions Executed", "0") or 0)
+        except ValueError:
+            d["_s"], d["_e"] = 0, 0
+    tot_s = sum(d["_s"] for d in data) or 1
+    tot_e = sum(d["_e"] for d in data) or 1
+    ops = collections.Counter()
+    ops_s = collections.Counter()
+    for d in data:
+        toks = d["Source"].strip().split(" ")
+        op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+        parts = op.split(".")
+        op = ".".join(parts[:2]) if parts[0] == "IMAD" else parts[0]     # IMAD.WIDE / .IADD / .MOV / .HI
+        ops[op] += d["_e"]
+        ops_s[op] += d["_s"]
+    with open(out, "w") as f:
+        f.write(det)
+        f.write("\n=== SASS opcode mix (executed warp instructions, share of stall samples) ===\n")
+        for op, e in ops.most_common(25):
+            f.write(f"{op:12s} exec {100 * e / tot_e:5.1f}%  stalls {100 * ops_s[op] / tot_s:5.1f}%\n")
+        f.write(f"\n=== top {top} SASS lines by stall samples (of {tot_s}) ===\n")
+        for d in sorted(data, key=lambda d: -d["_s"])[:top]:
+            f.write(f"{100 * d['_s'] / tot_s:5.2f}%  exec {d['_e']:>10d}  {d['Address'][-5:]}  {d['Source'].strip()[:90]}\n")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 60)
