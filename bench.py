@@ -827,10 +827,30 @@ def run_latency(args, local_rank, schedule="reference"):
     t0 = time.perf_counter()
     res = run_encrypted(net, plan, ws, xs[0], ctx=ctx)
     e2e_ms = 1e3 * (time.perf_counter() - t0)
-    ok = [int(v) for v in res.logits] == _oracle_logits(net, ws, xs)[0]
+    want = _oracle_logits(net, ws, xs)[0]
+    ok = [int(v) for v in res.logits] == want
+    # the same walk captured once as a CUDA graph and replayed (runner.CapturedPlan)
+    from paper_2102_03494_b200.runner import CapturedPlan
+    graph = {}
+    try:
+        cp = CapturedPlan(net, plan, ws, np.zeros_like(xs[0]), ctx)
+        cp.run(xs[0])                                               # warm replay
+        ev.sync()
+        e0.record(stream)
+        cp.replay()
+        e1.record(stream)
+        e1.synchronize()
+        g_dev = e0.elapsed_time(e1)
+        t0 = time.perf_counter()
+        lg = cp.run(xs[0])
+        g_e2e = 1e3 * (time.perf_counter() - t0)
+        graph = {"device_ms": g_dev, "e2e_ms": g_e2e, "nodes": cp.nodes,
+                 "logits_match": [int(v) for v in np.atleast_1d(lg)] == want}
+    except Exception as exc:                                        # noqa: BLE001 -- reported, not fatal
+        graph = {"error": str(exc)[:300]}
     return {"workload": "configs[0]: one 28x28 image (zero-padded to 29x29), batch 1", "schedule": schedule,
             "level_schedule": bool(args.level_schedule), "device_ms": dev_ms, "e2e_ms": e2e_ms,
-            "logits_match": ok, "crt_primes": rp.T, "L": rp.L}
+            "logits_match": ok, "crt_primes": rp.T, "L": rp.L, "graph_replay": graph}
 
 
 def _oracle_logits(net, ws, xs):

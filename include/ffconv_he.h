@@ -70,6 +70,7 @@ typedef struct fhe_params {
 typedef struct fhe_ctx fhe_ctx;
 typedef struct fhe_ct fhe_ct;
 typedef struct fhe_pt fhe_pt;
+typedef struct fhe_graph fhe_graph;
 
 const char *fhe_last_error(void);
 const char *fhe_backend_name(void);   /* "cuda-sm100a" or "golden-c" */
@@ -115,6 +116,24 @@ int fhe_ct_to_device(fhe_ctx *ctx, const fhe_ct *ct, void *dst);
 int fhe_ct_from_device(fhe_ctx *ctx, fhe_ct *ct, const void *src);
 /* transparent encryption of zero: (0, 0) */
 int fhe_ct_zero(fhe_ctx *ctx, fhe_ct *ct);
+
+/* D2D copy of the words of src into dst (same R and level), asynchronous */
+int fhe_ct_copy(fhe_ctx *ctx, const fhe_ct *src, fhe_ct *dst);
+
+/* ---- plan capture (the op sequence of a walk is data-independent) --------------
+ * fhe_capture_begin starts recording every launch of the context into a CUDA graph;
+ * ciphertexts created until fhe_capture_end come from a device arena of arena_bytes
+ * that the graph keeps (fixed addresses across replays).  Keys, plaintexts and
+ * workspaces must already exist (run the walk once first): creating them inside a
+ * capture fails.  fhe_graph_launch replays the recorded work on the context's stream;
+ * ciphertexts created during the capture hold the replay's results.
+ * fhe_ctx_peak_bytes: the largest ciphertext memory held at once (arena sizing). */
+int fhe_capture_begin(fhe_ctx *ctx, uint64_t arena_bytes);
+int fhe_capture_end(fhe_ctx *ctx, fhe_graph **out);
+int fhe_graph_launch(fhe_ctx *ctx, fhe_graph *graph);
+int fhe_graph_nodes(fhe_graph *graph, uint64_t *out);
+void fhe_graph_destroy(fhe_graph *graph);
+int fhe_ctx_peak_bytes(fhe_ctx *ctx, uint64_t *out, int reset);
 
 /* ---- plaintexts --------------------------------------------------------- */
 int fhe_pt_create(fhe_ctx *ctx, fhe_pt **out);

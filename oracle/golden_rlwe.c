@@ -754,6 +754,20 @@ int fhe_decrypt_slots(fhe_ctx *c, const fhe_ct *ct, uint32_t lo, uint32_t cnt, u
     return 0;
 }
 
+int fhe_ct_copy(fhe_ctx *c, const fhe_ct *src, fhe_ct *dst) {
+    if (src->R != dst->R || src->level != dst->level) return fail(FHE_ELEVEL, "ct_copy: shape/level mismatch");
+    memcpy(dst->data, src->data, (size_t)src->count * 2 * src->level * c->n * 8);
+    return 0;
+}
+
+/* plan capture is a device feature: the golden model evaluates eagerly */
+int fhe_capture_begin(fhe_ctx *c, uint64_t arena_bytes) { (void)c; (void)arena_bytes; return fail(FHE_EINVAL, "no device in the golden model"); }
+int fhe_capture_end(fhe_ctx *c, fhe_graph **out) { (void)c; *out = NULL; return fail(FHE_EINVAL, "no device in the golden model"); }
+int fhe_graph_launch(fhe_ctx *c, fhe_graph *g) { (void)c; (void)g; return fail(FHE_EINVAL, "no device in the golden model"); }
+int fhe_graph_nodes(fhe_graph *g, uint64_t *out) { (void)g; *out = 0; return fail(FHE_EINVAL, "no device in the golden model"); }
+void fhe_graph_destroy(fhe_graph *g) { (void)g; }
+int fhe_ctx_peak_bytes(fhe_ctx *c, uint64_t *out, int reset) { (void)c; (void)reset; *out = 0; return 0; }
+
 int fhe_check_zero_tail(fhe_ctx *c, const fhe_ct *ct, uint32_t m) {
     if (m > c->N) return fail(FHE_EINVAL, "check_zero_tail: m = %u exceeds %u slots", m, c->N);
     if (m == c->N) return 0;

@@ -69,6 +69,13 @@ SIGNATURES = {
     "fhe_ct_zero": (c_int, [c_void_p, c_void_p]),
     "fhe_ct_to_device": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fhe_ct_from_device": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "fhe_ct_copy": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "fhe_capture_begin": (c_int, [c_void_p, c_uint64]),
+    "fhe_capture_end": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "fhe_graph_launch": (c_int, [c_void_p, c_void_p]),
+    "fhe_graph_nodes": (c_int, [c_void_p, _U64P]),
+    "fhe_graph_destroy": (None, [c_void_p]),
+    "fhe_ctx_peak_bytes": (c_int, [c_void_p, _U64P, c_int]),
     "fhe_pt_create": (c_int, [c_void_p, POINTER(c_void_p)]),
     "fhe_pt_destroy": (None, [c_void_p]),
     "fhe_encode": (c_int, [c_void_p, _U64P, c_void_p]),

@@ -118,6 +118,8 @@ struct KeyBuf {
     u64 last = 0;       // key-use tick of the last launch sequence that referenced it
 };
 
+struct Arena;
+
 struct fhe_ctx {
     fhe_params P{};
     int dev = 0;
@@ -175,6 +177,11 @@ struct fhe_ctx {
     size_t w_sq_words = 0;
     u64 *w_tmp = nullptr;
     size_t w_tmp_words = 0;
+    // plan capture (fhe_capture_begin/end): allocations come from cap_arena, frees of
+    // pool memory are deferred to the end of the capture
+    Arena *cap_arena = nullptr;
+    std::vector<void *> deferred_free;
+    size_t live_bytes = 0, peak_bytes = 0;   // pool-allocated ciphertext bytes (arena sizing)
     // profiling
     bool prof = false;
     u64 launches = 0;
@@ -213,10 +220,29 @@ struct ProfScope {
     }
 };
 
+// Device memory of ciphertexts created while a plan walk is captured into a CUDA graph:
+// a bump arena with exact-size free lists (the graph replays the same addresses, so the
+// arena lives as long as the graph or any handle into it).
+struct Arena {
+    u64 *base = nullptr;
+    size_t words = 0, top = 0;
+    std::unordered_map<size_t, std::vector<u64 *>> free_blocks;
+    long refs = 0;                      // live ciphertext handles into the arena
+    bool orphaned = false;              // its graph was destroyed
+};
+
+struct fhe_graph {
+    fhe_ctx *ctx;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    Arena *arena = nullptr;
+};
+
 struct fhe_ct {
     fhe_ctx *ctx;
     u32 R, level, count;
     u64 *d;
+    Arena *arena;                       // non-null: arena memory (captured plan)
 };
 
 struct fhe_pt {
@@ -329,6 +355,7 @@ static void map_q(ModMap &m, u32 l) { map_range(m, l, 0); }
 
 static int ensure_tmp(fhe_ctx *c, size_t words) {
     if (words <= c->w_tmp_words) return 0;
+    if (c->cap_arena) return fail(FHE_EINVAL, "workspace growth inside a capture (warm the walk up first)");
     if (c->w_tmp) CU(cudaFreeAsync(c->w_tmp, c->st));
     CU(cudaMallocAsync((void **)&c->w_tmp, words * 8, c->st));
     c->w_tmp_words = words;
@@ -819,6 +846,7 @@ static int get_key(fhe_ctx *c, u32 kid, const u64 **out) {
         *out = it->second.d;
         return 0;
     }
+    if (c->cap_arena) return fail(FHE_EINVAL, "key for Galois element %u was not generated before the capture", kid);
     size_t n = c->n, L = c->L;
     size_t words = L * 2 * (L + 1) * n;
     TRY(evict_keys(c, words * 8));
@@ -868,23 +896,150 @@ extern "C" int fhe_keygen_rotations(fhe_ctx *c, const uint32_t *steps, uint32_t 
 }
 
 // ================================================================== objects
+static bool same_shape_rl(const fhe_ct *a, const fhe_ct *b) { return a->R == b->R && a->level == b->level; }
+
 extern "C" int fhe_ct_create(fhe_ctx *c, uint32_t R, uint32_t level, fhe_ct **out) {
     if (R < 1) return fail(FHE_EINVAL, "R must be >= 1");
     if (level < 1 || level > c->L) return fail(FHE_ELEVEL, "level %u outside [1, %u]", level, c->L);
-    fhe_ct *ct = new fhe_ct{c, R, level, R * c->T, nullptr};
-    cudaError_t e = cudaMallocAsync((void **)&ct->d, ct_words(ct) * 8, c->st);
+    fhe_ct *ct = new fhe_ct{c, R, level, R * c->T, nullptr, nullptr};
+    const size_t words = ct_words(ct);
+    if (Arena *a = c->cap_arena) {
+        auto &fl = a->free_blocks[words];
+        if (!fl.empty()) {
+            ct->d = fl.back();
+            fl.pop_back();
+        } else if (a->top + words <= a->words) {
+            ct->d = a->base + a->top;
+            a->top += (words + 31) & ~(size_t)31;            // 256-byte aligned blocks
+        } else {
+            delete ct;
+            return fail(FHE_ENOMEM, "capture arena exhausted (%zu words); capture with a larger arena", a->words);
+        }
+        ct->arena = a;
+        a->refs++;
+        *out = ct;
+        return 0;
+    }
+    cudaError_t e = cudaMallocAsync((void **)&ct->d, words * 8, c->st);
     if (e != cudaSuccess) {
         delete ct;
-        return fail(FHE_ENOMEM, "ciphertext allocation of %zu bytes failed: %s", (size_t)R * c->T * 2 * level * c->n * 8,
-                    cudaGetErrorString(e));
+        return fail(FHE_ENOMEM, "ciphertext allocation of %zu bytes failed: %s", words * 8, cudaGetErrorString(e));
     }
+    c->live_bytes += words * 8;
+    c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
     *out = ct;
     return 0;
 }
+static void arena_release(Arena *a) {
+    if (a->orphaned && a->refs == 0) {
+        cudaDeviceSynchronize();
+        cudaFree(a->base);
+        delete a;
+    }
+}
 extern "C" void fhe_ct_destroy(fhe_ct *ct) {
     if (!ct) return;
-    cudaFreeAsync(ct->d, ct->ctx->streams[0]);
+    fhe_ctx *c = ct->ctx;
+    if (Arena *a = ct->arena) {
+        // during its capture the block returns to the free list (later captured work
+        // reuses it in stream order); afterwards the graph keeps writing it
+        if (a == c->cap_arena) a->free_blocks[ct_words(ct)].push_back(ct->d);
+        a->refs--;
+        arena_release(a);
+    } else if (c->cap_arena) {
+        c->deferred_free.push_back(ct->d);               // no pool frees inside a capture
+        c->live_bytes -= ct_words(ct) * 8;
+    } else {
+        cudaFreeAsync(ct->d, c->streams[0]);
+        c->live_bytes -= ct_words(ct) * 8;
+    }
     delete ct;
+}
+
+extern "C" int fhe_ct_copy(fhe_ctx *c, const fhe_ct *src, fhe_ct *dst) {
+    if (!same_shape_rl(src, dst)) return fail(FHE_ELEVEL, "ct_copy: shape/level mismatch");
+    CU(cudaMemcpyAsync(dst->d, src->d, ct_words(src) * 8, cudaMemcpyDeviceToDevice, c->st));
+    return 0;
+}
+
+extern "C" int fhe_ctx_peak_bytes(fhe_ctx *c, uint64_t *out, int reset) {
+    *out = c->peak_bytes;
+    if (reset) c->peak_bytes = c->live_bytes;
+    return 0;
+}
+
+extern "C" int fhe_capture_begin(fhe_ctx *c, uint64_t arena_bytes) {
+    if (c->cap_arena) return fail(FHE_EINVAL, "capture_begin: a capture is already running");
+    if (c->prof) return fail(FHE_EINVAL, "capture_begin: profiling is on");
+    for (int k = 0; k < c->lanes; k++) CU(cudaStreamSynchronize(c->streams[k]));
+    Arena *a = new Arena();
+    a->words = arena_bytes / 8;
+    if (cudaMalloc((void **)&a->base, a->words * 8) != cudaSuccess) {
+        delete a;
+        cudaGetLastError();
+        return fail(FHE_ENOMEM, "capture arena of %llu bytes", (unsigned long long)arena_bytes);
+    }
+    cudaError_t e = cudaStreamBeginCapture(c->streams[0], cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) {
+        cudaFree(a->base);
+        delete a;
+        return fail(FHE_EDEVICE, "cudaStreamBeginCapture: %s", cudaGetErrorString(e));
+    }
+    c->st = c->streams[0];
+    c->cap_arena = a;
+    return 0;
+}
+
+extern "C" int fhe_capture_end(fhe_ctx *c, fhe_graph **out) {
+    Arena *a = c->cap_arena;
+    if (!a) return fail(FHE_EINVAL, "capture_end: no capture is running");
+    c->cap_arena = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->streams[0], &g);
+    for (void *p : c->deferred_free) cudaFreeAsync(p, c->streams[0]);
+    c->deferred_free.clear();
+    if (e != cudaSuccess || !g) {
+        a->orphaned = true;
+        arena_release(a);
+        return fail(FHE_EDEVICE, "cudaStreamEndCapture: %s (an operation in the walk is not capturable)",
+                    cudaGetErrorString(e));
+    }
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, g, 0);
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        a->orphaned = true;
+        arena_release(a);
+        return fail(FHE_EDEVICE, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+    }
+    size_t nodes = 0;
+    cudaGraphGetNodes(g, nullptr, &nodes);
+    *out = new fhe_graph{c, g, exec, a};
+    return 0;
+}
+
+extern "C" int fhe_graph_launch(fhe_ctx *c, fhe_graph *g) {
+    if (c->cap_arena) return fail(FHE_EINVAL, "graph_launch inside a capture");
+    ProfScope ps_(c, "graph");
+    CU(cudaGraphLaunch(g->exec, c->st));
+    return 0;
+}
+
+extern "C" int fhe_graph_nodes(fhe_graph *g, uint64_t *out) {
+    size_t n = 0;
+    if (cudaGraphGetNodes(g->g, nullptr, &n) != cudaSuccess) return fail(FHE_EDEVICE, "cudaGraphGetNodes");
+    *out = n;
+    return 0;
+}
+
+extern "C" void fhe_graph_destroy(fhe_graph *g) {
+    if (!g) return;
+    cudaStreamSynchronize(g->ctx->streams[0]);
+    cudaGraphExecDestroy(g->exec);
+    cudaGraphDestroy(g->g);
+    g->arena->orphaned = true;
+    arena_release(g->arena);
+    delete g;
 }
 extern "C" uint32_t fhe_ct_level(const fhe_ct *ct) { return ct->level; }
 extern "C" uint32_t fhe_ct_rows(const fhe_ct *ct) { return ct->R; }
@@ -915,6 +1070,7 @@ extern "C" int fhe_ct_zero(fhe_ctx *c, fhe_ct *ct) {
 }
 
 extern "C" int fhe_pt_create(fhe_ctx *c, fhe_pt **out) {
+    if (c->cap_arena) return fail(FHE_EINVAL, "plaintext creation inside a capture (warm the walk up first)");
     fhe_pt *pt = new fhe_pt{c, nullptr, nullptr, 0};
     size_t n = c->n;
     if (cudaMallocAsync((void **)&pt->coef_t, c->T * n * 8, c->st) != cudaSuccess ||
@@ -927,6 +1083,12 @@ extern "C" int fhe_pt_create(fhe_ctx *c, fhe_pt **out) {
 }
 extern "C" void fhe_pt_destroy(fhe_pt *pt) {
     if (!pt) return;
+    if (pt->ctx->cap_arena) {
+        pt->ctx->deferred_free.push_back(pt->coef_t);
+        pt->ctx->deferred_free.push_back(pt->ntt_m);
+        delete pt;
+        return;
+    }
     // stream 0 explicitly: a finalizer may run while a call has switched c->st to lane 1
     cudaFreeAsync(pt->coef_t, pt->ctx->streams[0]);
     cudaFreeAsync(pt->ntt_m, pt->ctx->streams[0]);

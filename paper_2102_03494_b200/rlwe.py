@@ -55,6 +55,20 @@ class Plaintext(_Handle):
         super().__init__(ptr.value, ev.lib.dll.fhe_pt_destroy, ev._keepalive)
 
 
+class Graph(_Handle):
+    """A captured launch sequence (CUDA graph) and the device arena it writes."""
+
+    __slots__ = ()
+
+    def __init__(self, ev: "Evaluator", ptr):
+        super().__init__(ptr, ev.lib.dll.fhe_graph_destroy, ev._keepalive)
+
+    def nodes(self, ev: "Evaluator") -> int:
+        v = ctypes.c_uint64()
+        ev.lib.call("fhe_graph_nodes", self.ptr, ctypes.byref(v))
+        return v.value
+
+
 class _CtxOwner:
     """Destroys the fhe_ctx once the evaluator and every handle are gone."""
 
@@ -290,6 +304,26 @@ class Evaluator:
                       handle_array([c.ptr for c in b]), handle_array([o.ptr for o in outs]),
                       len(a))
         return outs
+
+    def copy(self, src: Ciphertext, dst: Ciphertext) -> None:
+        """dst <- src words on the device (same rows and level), asynchronous."""
+        self.lib.call("fhe_ct_copy", self.ctx, src.ptr, dst.ptr)
+
+    def peak_bytes(self, reset: bool = False) -> int:
+        v = ctypes.c_uint64()
+        self.lib.call("fhe_ctx_peak_bytes", self.ctx, ctypes.byref(v), int(reset))
+        return v.value
+
+    def capture_begin(self, arena_bytes: int) -> None:
+        self.lib.call("fhe_capture_begin", self.ctx, int(arena_bytes))
+
+    def capture_end(self) -> "Graph":
+        ptr = ctypes.c_void_p()
+        self.lib.call("fhe_capture_end", self.ctx, ctypes.byref(ptr))
+        return Graph(self, ptr.value)
+
+    def launch(self, graph: "Graph") -> None:
+        self.lib.call("fhe_graph_launch", self.ctx, graph.ptr)
 
     def keygen_rotations(self, steps) -> None:
         arr = (ctypes.c_uint32 * len(steps))(*[int(s) for s in steps])

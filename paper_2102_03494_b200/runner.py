@@ -401,6 +401,60 @@ def run_encrypted(net: NetworkSpec, plan: PackingPlan, weights: WeightSet, input
                      ctx.elided_rotations, value)
 
 
+def _packed_cts(value):
+    if isinstance(value, DensePacked):
+        return [value.ct]
+    return list(value.cts)
+
+
+class CapturedPlan:
+    """One plan walk's device work, recorded once as a CUDA graph and replayed.
+
+    The op sequence of a walk is data-independent (the reference's count-only walk,
+    runner.py:290-293, proves it), so the launches of `run_encrypted` on a packed
+    input can be captured (fhe_capture_begin/end) and replayed for every new input of
+    the same shape: a replay copies the new encrypted input into the captured input
+    ciphertexts and launches the graph -- no Python plan walk, no per-op launches.
+    A warm-up walk first creates the keys, plaintexts and workspaces the capture
+    needs and measures the ciphertext memory the arena must hold.  Op counters and
+    depths are those of the captured walk (`self.result`)."""
+
+    def __init__(self, net: NetworkSpec, plan: PackingPlan, weights: WeightSet, example, ctx, *,
+                 mask_fc: bool = True, arena_margin: float = 1.25):
+        self.net, self.plan, self.weights, self.ctx = net, plan, weights, ctx
+        ev = ctx.evaluator
+        ev.peak_bytes(reset=True)
+        warm = pack_input(net, plan, example, ctx)
+        run_encrypted(net, plan, weights, None, ctx=ctx, packed=warm, decrypt=False, mask_fc=mask_fc)
+        ev.sync()
+        peak = ev.peak_bytes()
+        del warm
+        self.packed = pack_input(net, plan, example, ctx)      # the buffers the graph reads
+        ev.sync()
+        ev.capture_begin(int(peak * arena_margin) + (64 << 20))
+        try:
+            self.result = run_encrypted(net, plan, weights, None, ctx=ctx, packed=self.packed, decrypt=False,
+                                        mask_fc=mask_fc)
+        finally:
+            self.graph = ev.capture_end()
+        self.nodes = self.graph.nodes(ev)
+
+    def replay(self, packed=None):
+        """Run the captured walk on `packed` (same shape as the example's), or again
+        on the current contents of the captured input; returns the encrypted value."""
+        ev = self.ctx.evaluator
+        if packed is not None:
+            for dst, src in zip(_packed_cts(self.packed), _packed_cts(packed)):
+                ev.copy(src.handle, dst.handle)
+        ev.launch(self.graph)
+        return self.result.value
+
+    def run(self, images):
+        """Host images -> encrypt -> replay -> decrypted logits."""
+        self.replay(pack_input(self.net, self.plan, images, self.ctx))
+        return _logits(self.result.value, self.ctx)
+
+
 def _switch_value(value, ctx, level: int):
     """Modulus-switch every ciphertext of a packed value down to `level` (uncounted,
     as in hesim.HeContext.mod_switch)."""

@@ -188,3 +188,27 @@ def test_cfg0_level_schedule_on_gpu(cuda_lib, schedule):
     if schedule == "reference":
         c = res.counters
         assert (c.mul_pc, c.add_cc, c.rot, c.mul_cc, c.assembly_mul_pc) == (458, 4894, 4889, 2, 438)
+
+
+def test_captured_plan_replay_on_gpu(cuda_lib):
+    """Plan capture + CUDA-graph replay (runner.CapturedPlan): the walk is recorded once on
+    an all-zero example batch and replayed for new images; every replay decrypts to the
+    reference's logits, and the replay issues no per-op launches from Python."""
+    import ctypes
+    from paper_2102_03494_b200.runner import CapturedPlan
+    for fx in load("networks.json")[:4]:
+        net, ws = network_from_fixture(fx)
+        plan = build_plan(net, "explicit")
+        x = np.array(fx["inputs"])
+        ctx = HeContext(net.scheme, batch=2, lib=cuda_lib)
+        cp = CapturedPlan(net, plan, ws, np.zeros_like(x), ctx)
+        assert cp.nodes > 10
+        ev = ctx.evaluator
+        n0 = ctypes.c_uint64()
+        cuda_lib.call("fhe_launch_count", ev.ctx, ctypes.byref(n0))
+        got = cp.run(x)
+        n1 = ctypes.c_uint64()
+        cuda_lib.call("fhe_launch_count", ev.ctx, ctypes.byref(n1))
+        assert [[int(v) for v in row] for row in got] == fx["logits"]
+        assert [[int(v) for v in row] for row in cp.run(x[::-1].copy())] == fx["logits"][::-1]
+        assert n1.value - n0.value < 40        # encrypt + copy + one graph launch + decrypt
