@@ -1494,17 +1494,37 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
 template <int LOGN>
 static void launch_ks_fused(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsAdd &kad) {
     using F = KsfCfg<LOGN>;
-    const size_t smem = (size_t)F::C::SMEM_WORDS * sizeof(u64);
+    using C = typename F::C;
+    const size_t smem = (size_t)C::SMEM_WORDS * sizeof(u64);
+    auto kern = k_ks_fused<LOGN>;
     {
         std::lock_guard<std::mutex> lk(g_attr_mu);
-        if (!g_attr_done.count((const void *)k_ks_fused<LOGN>)) {
-            cudaFuncSetAttribute((const void *)k_ks_fused<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            g_attr_done.insert((const void *)k_ks_fused<LOGN>);
+        if (!g_attr_done.count((const void *)kern)) {
+            cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            g_attr_done.insert((const void *)kern);
         }
     }
     ProfScope ps_(c, "k_ks_fused");
-    k_ks_fused<LOGN><<<(unsigned)(S * (l + 1)), F::TH, smem, c->st>>>(dt, c->w_Acc, S, (int)l, (int)c->L, c->special_id,
-                                                                    c->d_mods, kad);
+    const unsigned items = (unsigned)(S * (l + 1));
+    if constexpr (C::CR == 1) {
+        kern<<<items, F::TH, smem, c->st>>>(dt, c->w_Acc, S, (int)l, (int)c->L, c->special_id, c->d_mods, kad);
+    } else {
+        // one thread-block cluster of CR CTAs per (ciphertext, prime): each CTA owns 2^14
+        // words of the row and their accumulators in its TMEM
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(items * C::CR);
+        cfg.blockDim = dim3(F::TH);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = c->st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C::CR;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, dt, c->w_Acc, S, (int)l, (int)c->L, c->special_id, (const ModInfo *)c->d_mods, kad);
+    }
 }
 
 // FHE_KS_FUSED=1 selects the fused path.  Off by default: bit-exact, but measured slower
@@ -1513,7 +1533,7 @@ static void launch_ks_fused(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const 
 // k_ks_inner accumulates l products in 128 bits and reduces once.
 static bool ks_fused_ok(const fhe_ctx *c) {
     const char *e = getenv("FHE_KS_FUSED");
-    return e && atoi(e) && c->logn >= 9 && c->logn <= 14;
+    return e && atoi(e) && c->logn >= 9 && c->logn <= 16;
 }
 
 static int keyswitch_fused(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsOut &ko) {
@@ -1534,7 +1554,9 @@ static int keyswitch_fused(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const K
         case 12: launch_ks_fused<12>(c, S, l, dt, kad); break;
         case 13: launch_ks_fused<13>(c, S, l, dt, kad); break;
         case 14: launch_ks_fused<14>(c, S, l, dt, kad); break;
-        default: return fail(FHE_EINVAL, "fused key switching needs 2^9 <= n <= 2^14");
+        case 15: launch_ks_fused<15>(c, S, l, dt, kad); break;
+        case 16: launch_ks_fused<16>(c, S, l, dt, kad); break;
+        default: return fail(FHE_EINVAL, "fused key switching needs 2^9 <= n <= 2^16");
     }
     CHECK_LAUNCH();
     // the special prime's accumulators to coefficient form, in place: row r = (s, p)

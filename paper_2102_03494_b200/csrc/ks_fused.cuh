@@ -68,21 +68,50 @@ DEV void tmem_st16(u32 ta, const u32 (&r)[16]) {
         : "memory");
 }
 
-// Row configuration of the fused kernel: single-CTA rows, at least one full warp
-// (tcgen05.ld/st are warp-collective), radix-32 passes from 2^12 (the ModUp radix).
+// 8 consecutive 32-bit columns (two accumulator pairs)
+DEV void tmem_ld8(u32 ta, u32 (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta)
+                 : "memory");
+}
+DEV void tmem_st8(u32 ta, const u32 (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(ta), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+template <int CH>
+DEV void tmem_ld(u32 ta, u32 (&r)[4 * CH]) {
+    if constexpr (CH == 4) tmem_ld16(ta, r);
+    else tmem_ld8(ta, r);
+}
+template <int CH>
+DEV void tmem_st(u32 ta, const u32 (&r)[4 * CH]) {
+    if constexpr (CH == 4) tmem_st16(ta, r);
+    else tmem_st8(ta, r);
+}
+
+// Row configuration of the fused kernel: the ModUp rows' configuration (radix-32
+// single-CTA rows from 2^12, radix-16 thread-block-cluster rows for 2^15 / 2^16, where
+// every CTA owns 2^14 words and keeps their accumulators in its own TMEM); at least one
+// full warp (tcgen05.ld/st are warp-collective).
 template <int LOGN>
 struct KsfCfg {
-    static_assert(LOGN >= 9 && LOGN <= 14, "fused key switching: single-CTA rows of 2^9 .. 2^14 words");
-    static constexpr int W = LOGN >= 12 ? 5 : 4;
-    using C = NttCfg<LOGN, W>;
-    static constexpr int E = C::E, TH = C::TH, N = C::N;
+    static_assert(LOGN >= 9 && LOGN <= 16, "fused key switching: rows of 2^9 .. 2^16 words");
+    static constexpr int WO = FwdW5<LOGN>::value;
+    using C = RowCfg<LOGN, false, WO>;
+    static constexpr int E = C::E, TH = C::TH, N = C::N, NL = C::NL, W = C::W;
     static constexpr int WARPS = TH / 32;
     static constexpr int COLS_PER_THREAD = 4 * E;                       // two u64 accumulators per word
     static constexpr int BLOCKS = (WARPS + 3) / 4;                      // column blocks (warps sharing a lane quarter)
     static constexpr int NEED = COLS_PER_THREAD * BLOCKS;
     static constexpr u32 NCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
     static_assert(NEED <= 512, "accumulators exceed TMEM");
-    static_assert(E % 4 == 0, "TMEM accesses move 4 words (16 columns) at a time");
+    // words per TMEM access: 4 (16 columns) with 128 registers per thread, 2 (8 columns)
+    // with 64 (the 1024-thread radix-16 rows)
+    static constexpr int CH = TH <= 512 ? 4 : 2;
+    static_assert(E % CH == 0, "TMEM accesses move CH words at a time");
+    static_assert(TH >= 32, "at least one full warp");
 };
 
 // acc_p += Mont(x_e, key_p[j][i]) for this thread's words x = tid + e TH.  DIAG: the
@@ -93,44 +122,45 @@ DEV void ksf_mac(u32 tbase, bool first, const u64 *sm, const u64 *dg, u32 dperm,
                  u64 q, u64 qinv, int tid) {
     using F = KsfCfg<LOGN>;
     using C = typename F::C;
-    constexpr int E = F::E, TH = F::TH;
-    // rolled over the 4-word chunks (the kernel's code must stay within the instruction
+    constexpr int E = F::E, TH = F::TH, CH = F::CH;
+    // rolled over the CH-word chunks (the kernel's code must stay within the instruction
     // cache next to the unrolled NTT passes); the chunk's key words are loaded before
     // its TMEM accumulators so both latencies overlap
 #pragma unroll 1
-    for (int c = 0; c < E / 4; c++) {
-        u64 xv[4], kv0[4], kv1[4];
+    for (int c = 0; c < E / CH; c++) {
+        u64 xv[CH], kv0[CH], kv1[CH];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int x = tid + (4 * c + k) * TH;
-            kv0[k] = __ldg(k0 + x);
-            kv1[k] = __ldg(k1 + x);
-            xv[k] = DIAG ? dg[dperm ? galois_perm((u32)x, dperm, LOGN) : (u32)x] : sm[C::pad(x)];
+        for (int k = 0; k < CH; k++) {
+            const int x = tid + (CH * c + k) * TH;                  // local word
+            const u32 gx = (u32)(C::base() + x);                      // word of the row
+            kv0[k] = __ldg(k0 + gx);
+            kv1[k] = __ldg(k1 + gx);
+            xv[k] = DIAG ? dg[dperm ? galois_perm(gx, dperm, LOGN) : gx] : sm[C::pad(x)];
         }
-        u32 r[16];
-        if (!first) tmem_ld16(tbase + 16 * c, r);
-        u64 p0[4], p1[4];
+        u32 r[4 * CH];
+        if (!first) tmem_ld<CH>(tbase + 4 * CH * c, r);
+        u64 p0[CH], p1[CH];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < CH; k++) {
             p0[k] = mont(xv[k], kv0[k], q, qinv);
             p1[k] = mont(xv[k], kv1[k], q, qinv);
         }
         if (!first) {
             tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
+            for (int k = 0; k < CH; k++) {
                 p0[k] = addm(((u64)r[4 * k + 1] << 32) | r[4 * k], p0[k], q);
                 p1[k] = addm(((u64)r[4 * k + 3] << 32) | r[4 * k + 2], p1[k], q);
             }
         }
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < CH; k++) {
             r[4 * k] = (u32)p0[k];
             r[4 * k + 1] = (u32)(p0[k] >> 32);
             r[4 * k + 2] = (u32)p1[k];
             r[4 * k + 3] = (u32)(p1[k] >> 32);
         }
-        tmem_st16(tbase + 16 * c, r);
+        tmem_st<CH>(tbase + 4 * CH * c, r);
     }
     tmem_wait_st();
 }
@@ -149,14 +179,14 @@ __global__ void __launch_bounds__(KsfCfg<LOGN>::TH, 1)
                const ModInfo *__restrict__ mods, const KsAdd ka) {
     using F = KsfCfg<LOGN>;
     using C = typename F::C;
-    constexpr int E = F::E, TH = F::TH, W = F::W;
+    constexpr int E = F::E, TH = F::TH, CH = F::CH;
     constexpr u32 n = F::N;
     extern __shared__ u64 sm[];
     __shared__ KsfItem it;
     const int tid = threadIdx.x, warp = tid >> 5;
     if (tid == 0) {
         // item: blocks [0, S) are the special-prime rows, then (s, i) for the q primes
-        const int b = blockIdx.x;
+        const int b = C::row();
         const int s = b < S ? b : (b - S) / l, i = b < S ? l : (b - S) % l;
         it.s = s;
         it.i = i;
@@ -191,8 +221,8 @@ __global__ void __launch_bounds__(KsfCfg<LOGN>::TH, 1)
             const u64 *src = it.coef + (u32)j * n;
             u64 v[E];
 #pragma unroll
-            for (int e = 0; e < E; e++) v[e] = centered_lift_lazy(src[(e << (LOGN - W)) | tid], half_j, qj_mod, M);
-            ntt_fwd_core<LOGN, W, false>(v, sm, M, tid);     // ends with __syncthreads
+            for (int e = 0; e < E; e++) v[e] = centered_lift_lazy(src[C::io(tid, e)], half_j, qj_mod, M);
+            ntt_fwd_row<LOGN, false, F::WO>(v, sm, M, tid);   // ends with __syncthreads
         }
         const ModInfo &Mq = mods[it.i == l ? special_id : it.i];
         const u64 *k0 = krow(j);
@@ -215,16 +245,16 @@ __global__ void __launch_bounds__(KsfCfg<LOGN>::TH, 1)
         u64 *o0 = Acc + ((u32)s * 2 * (l + 1) + (u32)i) * n;
         u64 *o1 = o0 + (u32)(l + 1) * n;
 #pragma unroll 1
-        for (int c = 0; c < E / 4; c++) {
-            u32 r[16];
-            tmem_ld16(tbase + 16 * c, r);
+        for (int c = 0; c < E / CH; c++) {
+            u32 r[4 * CH];
+            tmem_ld<CH>(tbase + 4 * CH * c, r);
             tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int x = tid + (4 * c + k) * TH;
+            for (int k = 0; k < CH; k++) {
+                const u32 x = (u32)(C::base() + tid + (CH * c + k) * TH);
                 u64 a0 = ((u64)r[4 * k + 1] << 32) | r[4 * k], a1 = ((u64)r[4 * k + 3] << 32) | r[4 * k + 2];
                 if (ad) {
-                    const u32 xa = ag ? galois_perm((u32)x, ag, LOGN) : (u32)x;
+                    const u32 xa = ag ? galois_perm(x, ag, LOGN) : x;
                     if (pmask & 1) a0 = addm(a0, mont(ad[(u32)i * n + xa], pr, q, qinv), q);
                     if (pmask & 2) a1 = addm(a1, mont(ad[aps + (u32)i * n + xa], pr, q, qinv), q);
                 }
@@ -243,13 +273,13 @@ __global__ void __launch_bounds__(KsfCfg<LOGN>::TH, 1)
         u64 *o0 = Acc + ((u32)s * 2 * (l + 1) + (u32)l) * n;
         u64 *o1 = o0 + (u32)(l + 1) * n;
 #pragma unroll 1
-        for (int c = 0; c < E / 4; c++) {
-            u32 r[16];
-            tmem_ld16(tbase + 16 * c, r);
+        for (int c = 0; c < E / CH; c++) {
+            u32 r[4 * CH];
+            tmem_ld<CH>(tbase + 4 * CH * c, r);
             tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int x = tid + (4 * c + k) * TH;
+            for (int k = 0; k < CH; k++) {
+                const u32 x = (u32)(C::base() + tid + (CH * c + k) * TH);
                 o0[x] = ((u64)r[4 * k + 1] << 32) | r[4 * k];
                 o1[x] = ((u64)r[4 * k + 3] << 32) | r[4 * k + 2];
             }
