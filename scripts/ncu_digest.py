@@ -16,6 +16,17 @@ def main(rep, out, top=60):
     det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    raw_keep = {}
+    if len(rr) >= 3:
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                  "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                  "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+                  "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__cycles_active.avg",
+                  "sm__cycles_elapsed.avg", "lts__t_sector_hit_rate.pct"):
+            if k in rr[0]:
+                raw_keep[k] = (rr[-1][rr[0].index(k)], rr[1][rr[0].index(k)])
     rows = list(csv.reader(src.splitlines()))
     hdr = None
     data = []
@@ -45,6 +56,9 @@ def main(rep, out, top=60):
         ops_s[op] += d["_s"]
     with open(out, "w") as f:
         f.write(det)
+        f.write("\n=== raw metrics ===\n")
+        for k, (v, unit) in raw_keep.items():
+            f.write(f"{k}    {v} {unit}\n")
         f.write("\n=== SASS opcode mix (executed warp instructions, share of stall samples) ===\n")
         for op, e in ops.most_common(25):
             f.write(f"{op:12s} exec {100 * e / tot_e:5.1f}%  stalls {100 * ops_s[op] / tot_s:5.1f}%\n")
