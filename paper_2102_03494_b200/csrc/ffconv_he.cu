@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
+#include <map>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -221,14 +223,39 @@ struct ProfScope {
 };
 
 // Device memory of ciphertexts created while a plan walk is captured into a CUDA graph:
-// a bump arena with exact-size free lists (the graph replays the same addresses, so the
-// arena lives as long as the graph or any handle into it).
+// one device slab with a best-fit extent allocator (free extents split and coalesce, so
+// the mixed ciphertext sizes of a level-scheduled walk reuse each other's memory).  The
+// graph replays the same addresses, so the arena lives as long as the graph or any
+// handle into it.
 struct Arena {
     u64 *base = nullptr;
-    size_t words = 0, top = 0;
-    std::unordered_map<size_t, std::vector<u64 *>> free_blocks;
+    size_t words = 0;
+    std::map<size_t, size_t> free_ext;  // offset -> length (words), disjoint, coalesced
     long refs = 0;                      // live ciphertext handles into the arena
     bool orphaned = false;              // its graph was destroyed
+    static size_t round(size_t w) { return (w + 31) & ~(size_t)31; }     // 256-byte blocks
+    u64 *alloc(size_t w) {
+        w = round(w);
+        auto best = free_ext.end();
+        for (auto it = free_ext.begin(); it != free_ext.end(); ++it)
+            if (it->second >= w && (best == free_ext.end() || it->second < best->second)) best = it;
+        if (best == free_ext.end()) return nullptr;
+        const size_t off = best->first, len = best->second;
+        free_ext.erase(best);
+        if (len > w) free_ext[off + w] = len - w;
+        return base + off;
+    }
+    void release(u64 *p, size_t w) {
+        w = round(w);
+        size_t off = (size_t)(p - base);
+        auto nx = free_ext.lower_bound(off);
+        if (nx != free_ext.begin()) {
+            auto pv = std::prev(nx);
+            if (pv->first + pv->second == off) { off = pv->first; w += pv->second; free_ext.erase(pv); }
+        }
+        if (nx != free_ext.end() && off + w == nx->first) { w += nx->second; free_ext.erase(nx); }
+        free_ext[off] = w;
+    }
 };
 
 struct fhe_graph {
@@ -904,14 +931,8 @@ extern "C" int fhe_ct_create(fhe_ctx *c, uint32_t R, uint32_t level, fhe_ct **ou
     fhe_ct *ct = new fhe_ct{c, R, level, R * c->T, nullptr, nullptr};
     const size_t words = ct_words(ct);
     if (Arena *a = c->cap_arena) {
-        auto &fl = a->free_blocks[words];
-        if (!fl.empty()) {
-            ct->d = fl.back();
-            fl.pop_back();
-        } else if (a->top + words <= a->words) {
-            ct->d = a->base + a->top;
-            a->top += (words + 31) & ~(size_t)31;            // 256-byte aligned blocks
-        } else {
+        ct->d = a->alloc(words);
+        if (!ct->d) {
             delete ct;
             return fail(FHE_ENOMEM, "capture arena exhausted (%zu words); capture with a larger arena", a->words);
         }
@@ -943,7 +964,7 @@ extern "C" void fhe_ct_destroy(fhe_ct *ct) {
     if (Arena *a = ct->arena) {
         // during its capture the block returns to the free list (later captured work
         // reuses it in stream order); afterwards the graph keeps writing it
-        if (a == c->cap_arena) a->free_blocks[ct_words(ct)].push_back(ct->d);
+        if (a == c->cap_arena) a->release(ct->d, ct_words(ct));
         a->refs--;
         arena_release(a);
     } else if (c->cap_arena) {
@@ -973,7 +994,8 @@ extern "C" int fhe_capture_begin(fhe_ctx *c, uint64_t arena_bytes) {
     if (c->prof) return fail(FHE_EINVAL, "capture_begin: profiling is on");
     for (int k = 0; k < c->lanes; k++) CU(cudaStreamSynchronize(c->streams[k]));
     Arena *a = new Arena();
-    a->words = arena_bytes / 8;
+    a->words = arena_bytes / 8 & ~(size_t)31;
+    a->free_ext[0] = a->words;
     if (cudaMalloc((void **)&a->base, a->words * 8) != cudaSuccess) {
         delete a;
         cudaGetLastError();
@@ -1389,7 +1411,7 @@ static void launch_modup_persist(fhe_ctx *c, int S, u32 l, const DigitTab &dt) {
 static int keyswitch_modup(fhe_ctx *c, int S, u32 l, const DigitTab &dt) {
     static int persist = -1;     // FHE_MODUP_PERSIST: persistent ModUp CTAs (single-CTA rows)
     if (persist < 0) { const char *e = getenv("FHE_MODUP_PERSIST"); persist = e ? atoi(e) : 1; }
-    if (persist && c->logn <= 14 && c->logn >= 12) {
+    if (persist && c->logn <= 14 && c->logn >= 12 && c->logn <= NTT_LOGL) {
         if (c->logn == 14) launch_modup_persist<14>(c, S, l, dt);
         else if (c->logn == 13) launch_modup_persist<13>(c, S, l, dt);
         else launch_modup_persist<12>(c, S, l, dt);

@@ -279,9 +279,9 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k
                                                                      int special_id, int rows,
                                                                      const ModInfo *__restrict__ mods) {
     using C = RowCfg<LOGN, false, FwdW5<LOGN>::value>;
-    static_assert(C::CL == 0, "persistent ModUp: single-CTA rows only");
     extern __shared__ u64 sm[];
     const int tid = threadIdx.x, ll = l * l;
+    if constexpr (C::CL != 0) return;     // single-CTA rows only (the host launches k_modup otherwise)
     for (int r = blockIdx.x; r < rows; r += gridDim.x) {
         const int s = r / ll, rem = r % ll, j = rem / l, ii = rem % l, i = ii < j ? ii : ii + 1;
         const int rn = r + gridDim.x;

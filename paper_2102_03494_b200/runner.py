@@ -431,12 +431,26 @@ class CapturedPlan:
         del warm
         self.packed = pack_input(net, plan, example, ctx)      # the buffers the graph reads
         ev.sync()
-        ev.capture_begin(int(peak * arena_margin) + (64 << 20))
-        try:
-            self.result = run_encrypted(net, plan, weights, None, ctx=ctx, packed=self.packed, decrypt=False,
-                                        mask_fc=mask_fc)
-        finally:
-            self.graph = ev.capture_end()
+        # the arena's extents split and coalesce, so the walk's peak plus a margin holds it;
+        # a walk that still outgrows it is captured again with a larger arena
+        for attempt in range(3):
+            ev.capture_begin(int(peak * arena_margin * (1 << attempt)) + (64 << 20))
+            err = None
+            try:
+                self.result = run_encrypted(net, plan, weights, None, ctx=ctx, packed=self.packed, decrypt=False,
+                                            mask_fc=mask_fc)
+            except Exception as e:          # noqa: BLE001 - re-raised below unless it is the arena
+                err = e
+            finally:
+                try:
+                    self.graph = ev.capture_end()
+                except Exception:           # noqa: BLE001 - the walk's own error is the one to report
+                    if err is None:
+                        raise
+            if err is None:
+                break
+            if "arena exhausted" not in str(err) or attempt == 2:
+                raise err
         self.nodes = self.graph.nodes(ev)
 
     def replay(self, packed=None):
