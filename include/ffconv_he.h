@@ -18,6 +18,9 @@
  *   fhe_add_plain     <- HeContext.add_plain         hesim.py:318-326
  *   fhe_square        <- HeContext.square            hesim.py:328-345
  *   fhe_mod_switch    <- (no reference counterpart; BASELINE cfg1 "rescale")
+ *   fhe_rotate_and_sum <- HeContext.rotate_and_sum   hesim.py:347-366
+ *   fhe_combine       <- combine_to_dense            packing.py:350-368
+ *   fhe_ct_gemm       <- conv_conv channel sums      engine.py:178-197
  *
  * Scheme: RNS-BFV over Z[X]/(X^n+1).  One ciphertext "slot row" of the reference
  * (n_slots = N) is one batching row of a ring of degree n = 2N; row 0 and row 1
@@ -208,6 +211,25 @@ int fhe_rotate_multi(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, const u
 int fhe_rotate_hoisted(fhe_ctx *ctx, const fhe_ct *a, const uint32_t *k, uint32_t m, fhe_ct *const *out);
 int fhe_mul_plain_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_pt *const *pt, fhe_ct *const *out, uint32_t m);
 int fhe_add_many(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *b, fhe_ct *const *out, uint32_t m);
+
+/* ---- composite operators (one call per reference operator) ------------
+ * rotate_and_sum (hesim.py:347-366) of m same-level objects: slot 0 of out[i] <- sum of
+ * the first span slots of a[i]; ceil(log2 span) levels acc += rotate(acc, 2^h),
+ * h = rounds-1 .. 0, each level ONE fused rotate-and-add launch sequence over all m
+ * objects.  Words equal the fhe_rotate / fhe_add sequence.  out[i] must not alias a[i]. */
+int fhe_rotate_and_sum(fhe_ctx *ctx, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t span);
+/* combine_to_dense (packing.py:350-368) as a pairwise tree: m slot-0-anchored payloads of
+ * lengths[i] slots are concatenated in order; every level merges adjacent blocks
+ * (left, right) into left + rotate(right, N - len(left)) with the addition fused into
+ * the key-switching epilogue, an odd last block moves up unchanged.  m - 1 rotations
+ * and additions (the reference's counts), one Galois key per distinct left length.
+ * sum(lengths) <= N; out must not alias an input. */
+int fhe_combine(fhe_ctx *ctx, fhe_ct *const *cts, const uint32_t *lengths, uint32_t m, fhe_ct *out);
+/* ct-GEMM, the ConvPack channel sums (engine.py:178-197): out[o] = sum_k w[k*O + o] * a[k]
+ * for o < O over K same-shape inputs, integer weights reduced per prime; every input
+ * word is read once per tile of 8 outputs.  Words equal the fhe_mul_scalar / fhe_add
+ * sequence.  out must not alias an input. */
+int fhe_ct_gemm(fhe_ctx *ctx, fhe_ct *const *a, uint32_t K, const int64_t *w, uint32_t O, fhe_ct *const *out);
 
 #ifdef __cplusplus
 }

@@ -1169,3 +1169,92 @@ int fhe_add_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *b, fhe_ct *const *
     for (u32 i = 0; i < m; i++) { int rc = fhe_add(c, a[i], b[i], out[i]); if (rc) return rc; }
     return 0;
 }
+
+/* ---- composite entry points (same words as the sequences they stand for) ---- */
+
+/* hesim.py:347-366: acc <- acc + rotate(acc, 2^h) for h = ceil(log2 span) - 1 .. 0 */
+int fhe_rotate_and_sum(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t span) {
+    if (span < 1 || span > c->N) return fail(FHE_EINVAL, "rotate_and_sum: span %u outside [1, %u]", span, c->N);
+    u32 rounds = 0;
+    while ((1u << rounds) < span) rounds++;
+    for (u32 i = 0; i < m; i++) {
+        if (!same_shape(a[i], out[i])) return fail(FHE_ELEVEL, "rotate_and_sum: shape/level mismatch");
+        if (a[i] == out[i]) return fail(FHE_EINVAL, "rotate_and_sum: out must not alias the input");
+        fhe_ct *tmp = NULL;
+        int rc = fhe_ct_create(c, a[i]->R, a[i]->level, &tmp);
+        if (rc) return rc;
+        memcpy(out[i]->data, a[i]->data, ct_words(a[i]) * 8);
+        for (u32 h = rounds; h-- > 0 && !rc;) {
+            rc = fhe_rotate(c, out[i], 1u << h, tmp);
+            if (!rc) rc = fhe_add(c, out[i], tmp, out[i]);
+        }
+        fhe_ct_destroy(tmp);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+/* packing.py:350-368 as a pairwise tree: every level merges adjacent blocks (left, right)
+ * into left + rotate(right, N - len(left)); an odd last block moves up unchanged. */
+int fhe_combine(fhe_ctx *c, fhe_ct *const *cts, const uint32_t *lengths, uint32_t m, fhe_ct *out) {
+    if (m < 1) return fail(FHE_EINVAL, "combine: no ciphertexts");
+    u64 total = 0;
+    for (u32 i = 0; i < m; i++) {
+        if (!same_shape(cts[i], out)) return fail(FHE_ELEVEL, "combine: shape/level mismatch");
+        if (cts[i] == out) return fail(FHE_EINVAL, "combine: out must not alias an input");
+        if (lengths[i] < 1) return fail(FHE_EINVAL, "combine: payload %u is empty", i);
+        total += lengths[i];
+    }
+    if (total > c->N) return fail(FHE_EINVAL, "combine: payload of %llu slots exceeds %u", (unsigned long long)total, c->N);
+    fhe_ct **cur = (fhe_ct **)malloc(m * sizeof *cur);
+    u32 *len = (u32 *)malloc(m * sizeof *len);
+    char *own = (char *)calloc(m, 1);          /* 1: a temporary of this call */
+    for (u32 i = 0; i < m; i++) { cur[i] = cts[i]; len[i] = lengths[i]; }
+    u32 cnt = m;
+    int rc = 0;
+    while (cnt > 1 && !rc) {
+        u32 w = 0;
+        for (u32 k = 0; k + 1 < cnt && !rc; k += 2) {
+            fhe_ct *dst = NULL;
+            if (cnt == 2) dst = out;
+            else rc = fhe_ct_create(c, out->R, out->level, &dst);
+            if (rc) break;
+            rc = fhe_rotate(c, cur[k + 1], c->N - len[k], dst);
+            if (!rc) rc = fhe_add(c, cur[k], dst, dst);
+            if (own[k]) fhe_ct_destroy(cur[k]);
+            if (own[k + 1]) fhe_ct_destroy(cur[k + 1]);
+            cur[w] = dst; len[w] = len[k] + len[k + 1]; own[w] = dst != out; w++;
+        }
+        if (!rc && (cnt & 1)) { cur[w] = cur[cnt - 1]; len[w] = len[cnt - 1]; own[w] = own[cnt - 1]; w++; }
+        cnt = w;
+    }
+    if (!rc && m == 1) memcpy(out->data, cts[0]->data, ct_words(out) * 8);
+    free(cur); free(len); free(own);
+    return rc;
+}
+
+/* engine.py:178-197 (conv_conv): out[o] = sum_k w[k * O + o] * a[k] */
+int fhe_ct_gemm(fhe_ctx *c, fhe_ct *const *a, uint32_t K, const int64_t *w, uint32_t O, fhe_ct *const *out) {
+    if (K < 1 || O < 1) return fail(FHE_EINVAL, "ct_gemm: empty operand list");
+    for (u32 k = 0; k < K; k++)
+        if (!same_shape(a[k], a[0])) return fail(FHE_ELEVEL, "ct_gemm: shape/level mismatch");
+    for (u32 o = 0; o < O; o++) {
+        if (!same_shape(out[o], a[0])) return fail(FHE_ELEVEL, "ct_gemm: shape/level mismatch");
+        for (u32 k = 0; k < K; k++)
+            if (out[o] == a[k]) return fail(FHE_EINVAL, "ct_gemm: out must not alias an input");
+    }
+    for (u32 o = 0; o < O; o++)
+        for (u32 ci = 0; ci < a[0]->count; ci++)
+            for (u32 p = 0; p < 2; p++)
+                for (u32 i = 0; i < a[0]->level; i++) {
+                    u64 q = c->P.q[i];
+                    u64 *z = poly(out[o], ci, p, i);
+                    memset(z, 0, (size_t)c->n * 8);
+                    for (u32 k = 0; k < K; k++) {
+                        u64 s = smod(w[(size_t)k * O + o], q);
+                        const u64 *x = poly(a[k], ci, p, i);
+                        for (u32 j = 0; j < c->n; j++) z[j] = addmod(z[j], mulmod(x[j], s, q), q);
+                    }
+                }
+    return 0;
+}

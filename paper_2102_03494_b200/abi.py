@@ -101,6 +101,9 @@ SIGNATURES = {
     "fhe_mul_plain_many": (c_int, [c_void_p, _VPP, _VPP, _VPP, c_uint32]),
     "fhe_hoisted_dot": (c_int, [c_void_p, _VPP, POINTER(c_uint32), c_uint32, _VPP, c_uint32, _VPP]),
     "fhe_add_many": (c_int, [c_void_p, _VPP, _VPP, _VPP, c_uint32]),
+    "fhe_rotate_and_sum": (c_int, [c_void_p, _VPP, _VPP, c_uint32, c_uint32]),
+    "fhe_combine": (c_int, [c_void_p, _VPP, POINTER(c_uint32), c_uint32, c_void_p]),
+    "fhe_ct_gemm": (c_int, [c_void_p, _VPP, c_uint32, POINTER(c_int64), c_uint32, _VPP]),
 }
 
 

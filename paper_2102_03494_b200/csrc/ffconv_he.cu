@@ -188,6 +188,8 @@ struct fhe_ctx {
     bool prof = false;
     u64 launches = 0;
     double alg_mm = 0;                  // algorithmic modmuls issued (fhe_work_modmuls)
+    // ct-GEMM weight tables ([L][K][O] residues, Montgomery form), keyed by content
+    std::unordered_map<u64, u64 *> gemm_tabs;
     struct Rec { const char *name; cudaEvent_t a, b; };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> ev_pool;
@@ -707,6 +709,7 @@ extern "C" void fhe_ctx_destroy(fhe_ctx *c) {
     cudaSetDevice(c->dev);
     if (c->st) cudaStreamSynchronize(c->st);
     for (auto &kv : c->keys) cudaFree(kv.second.d);
+    for (auto &kv : c->gemm_tabs) cudaFree(kv.second);
     for (u64 *d : c->key_free) cudaFree(d);
     for (int j = 0; j < 2; j++) {
         if (c->enc_stage[j]) cudaFreeHost(c->enc_stage[j]);
@@ -1622,8 +1625,10 @@ static void use_lane(fhe_ctx *c, int k) {
 // Galois element g[i].  Sub-batches alternate between two streams with their
 // own workspaces so the small-grid steps of one (ModDown INTT) overlap the
 // next one's ModUp.
+// addend: when non-null, addend[i] ([2][l][n], e.g. the input itself for a rotate-and-sum
+// level, or the left block of a combine merge) is added to output i in the epilogue.
 static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std::vector<u64 *> &out, u32 l,
-                       const std::vector<u32> &g, bool add_input = false) {
+                       const std::vector<u32> &g, const std::vector<const u64 *> *addend = nullptr) {
     std::vector<const u64 *> keys(in.size());
     size_t n = c->n;
     // (profiling runs single-stream so every kernel is timed in isolation)
@@ -1677,7 +1682,7 @@ static int rotate_phys(fhe_ctx *c, const std::vector<const u64 *> &in, const std
             ko.out[s] = out[b0 + s];
             ko.add[s] = in[b0 + s];          // c0 limbs, read through the automorphism
             ko.add_g[s] = g[b0 + s];
-            ko.acc[s] = add_input ? in[b0 + s] : nullptr;
+            ko.acc[s] = addend ? (*addend)[b0 + s] : nullptr;
         }
         ko.acc_pstride = (long long)l * n;
         ko.out_pstride = (long long)l * n;
@@ -1738,7 +1743,7 @@ extern "C" int fhe_rotate_add_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *
         size_t stride = 2ull * l * c->n;
         for (u32 ci = 0; ci < a[h]->count; ci++) { in.push_back(a[h]->d + ci * stride); o.push_back(out[h]->d + ci * stride); }
     }
-    return rotate_phys(c, in, o, l, std::vector<u32>(in.size(), galois_elt(c, k)), true);
+    return rotate_phys(c, in, o, l, std::vector<u32>(in.size(), galois_elt(c, k)), &in);
 }
 
 extern "C" int fhe_rotate_multi(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, const uint32_t *k, uint32_t m) {
@@ -1893,6 +1898,165 @@ extern "C" int fhe_add_many(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *b, fhe_
         k_add_many<<<dim3(bx, 1, i1 - i0), 256, 0, c->st>>>(t, total, (int)a[i0]->level, (int)c->logn, c->d_mods);
         CHECK_LAUNCH();
         i0 = i1;
+    }
+    return 0;
+}
+
+// ------------------------------------------------------ composite operators
+// rotate_and_sum of m objects: every tree level is one fused rotate-and-add launch
+// sequence over all physical ciphertexts (reference hesim.py:347-366)
+extern "C" int fhe_rotate_and_sum(fhe_ctx *c, fhe_ct *const *a, fhe_ct *const *out, uint32_t m, uint32_t span) {
+    if (span < 1 || span > c->N) return fail(FHE_EINVAL, "rotate_and_sum: span %u outside [1, %u]", span, c->N);
+    if (!m) return 0;
+    const u32 l = a[0]->level;
+    for (u32 h = 0; h < m; h++) {
+        if (a[h]->level != l || !same_shape(a[h], out[h])) return fail(FHE_ELEVEL, "rotate_and_sum: shape/level mismatch");
+        if (a[h]->d == out[h]->d) return fail(FHE_EINVAL, "rotate_and_sum: out must not alias the input");
+    }
+    u32 rounds = 0;
+    while ((1u << rounds) < span) rounds++;
+    if (!rounds) {
+        for (u32 h = 0; h < m; h++) TRY(fhe_ct_copy(c, a[h], out[h]));
+        return 0;
+    }
+    // levels alternate between out and one set of temporaries so the last one lands in out
+    std::vector<fhe_ct *> tmp(rounds > 1 ? m : 0, nullptr);
+    int rc = 0;
+    for (u32 h = 0; h < tmp.size() && !rc; h++) rc = fhe_ct_create(c, a[h]->R, l, &tmp[h]);
+    const size_t stride = 2ull * l * c->n;
+    for (u32 r = 0; r < rounds && !rc; r++) {
+        const bool to_out = (rounds - r) & 1;
+        std::vector<const u64 *> in;
+        std::vector<u64 *> o;
+        for (u32 h = 0; h < m; h++) {
+            const u64 *src = r == 0 ? a[h]->d : (to_out ? tmp[h]->d : out[h]->d);
+            u64 *dst = to_out ? out[h]->d : tmp[h]->d;
+            for (u32 ci = 0; ci < a[h]->count; ci++) { in.push_back(src + ci * stride); o.push_back(dst + ci * stride); }
+        }
+        rc = rotate_phys(c, in, o, l, std::vector<u32>(in.size(), galois_elt(c, 1u << (rounds - 1 - r))), &in);
+    }
+    for (fhe_ct *t : tmp) fhe_ct_destroy(t);
+    return rc;
+}
+
+// Tree concatenation of slot-0-anchored payloads (reference packing.py:350-368): every
+// level merges adjacent blocks as left + rotate(right, N - len(left)), all merges of a
+// level in one key-switching launch sequence with the addition in its epilogue.
+extern "C" int fhe_combine(fhe_ctx *c, fhe_ct *const *cts, const uint32_t *lengths, uint32_t m, fhe_ct *out) {
+    if (m < 1) return fail(FHE_EINVAL, "combine: no ciphertexts");
+    u64 total = 0;
+    for (u32 i = 0; i < m; i++) {
+        if (!same_shape(cts[i], out)) return fail(FHE_ELEVEL, "combine: shape/level mismatch");
+        if (cts[i]->d == out->d) return fail(FHE_EINVAL, "combine: out must not alias an input");
+        if (lengths[i] < 1) return fail(FHE_EINVAL, "combine: payload %u is empty", i);
+        total += lengths[i];
+    }
+    if (total > c->N) return fail(FHE_EINVAL, "combine: payload of %llu slots exceeds %u", (unsigned long long)total, c->N);
+    if (m == 1) return fhe_ct_copy(c, cts[0], out);
+    struct Item { fhe_ct *ct; u32 len; bool own; };
+    std::vector<Item> cur;
+    for (u32 i = 0; i < m; i++) cur.push_back({cts[i], lengths[i], false});
+    const u32 l = out->level;
+    const size_t stride = 2ull * l * c->n;
+    int rc = 0;
+    while (cur.size() > 1 && !rc) {
+        std::vector<Item> next;
+        std::vector<const u64 *> in, left;
+        std::vector<u64 *> o;
+        std::vector<u32> g;
+        for (size_t k = 0; k + 1 < cur.size() && !rc; k += 2) {
+            fhe_ct *dst = out;
+            if (cur.size() > 2) rc = fhe_ct_create(c, out->R, l, &dst);
+            if (rc) break;
+            const u32 ge = galois_elt(c, c->N - cur[k].len);
+            for (u32 ci = 0; ci < out->count; ci++) {
+                in.push_back(cur[k + 1].ct->d + ci * stride);
+                left.push_back(cur[k].ct->d + ci * stride);
+                o.push_back(dst->d + ci * stride);
+                g.push_back(ge);
+            }
+            next.push_back({dst, cur[k].len + cur[k + 1].len, dst != out});
+        }
+        if (!rc) rc = rotate_phys(c, in, o, l, g, &left);
+        if (rc)
+            for (auto &it : next)
+                if (it.own) fhe_ct_destroy(it.ct);
+        const size_t paired = cur.size() & ~(size_t)1;
+        for (size_t k = 0; k < paired; k++)
+            if (cur[k].own) fhe_ct_destroy(cur[k].ct);        // stream-ordered: the level above was enqueued
+        if (rc) {
+            if ((cur.size() & 1) && cur.back().own) fhe_ct_destroy(cur.back().ct);
+            break;
+        }
+        if (cur.size() & 1) next.push_back(cur.back());
+        cur.swap(next);
+    }
+    return rc;
+}
+
+// ct-GEMM (reference engine.py:178-197): out[o] = sum_k w[k O + o] a[k]
+static int gemm_table(fhe_ctx *c, const int64_t *w, u32 K, u32 O, const u64 **tab) {
+    u64 h = 1469598103934665603ull;
+    auto mix = [&](u64 v) { for (int b = 0; b < 8; b++) { h ^= (v >> (8 * b)) & 0xFF; h *= 1099511628211ull; } };
+    mix(K); mix(O);
+    for (size_t e = 0; e < (size_t)K * O; e++) mix((u64)w[e]);
+    auto it = c->gemm_tabs.find(h);
+    if (it != c->gemm_tabs.end()) { *tab = it->second; return 0; }
+    if (c->cap_arena) return fail(FHE_EINVAL, "ct_gemm weight table created inside a capture (warm the walk up first)");
+    const u32 L = c->L;
+    std::vector<u64> host((size_t)L * K * O);
+    for (u32 i = 0; i < L; i++) {
+        const u64 q = c->P.q[i];
+        for (size_t e = 0; e < (size_t)K * O; e++) {
+            const int64_t v = w[e];
+            const u64 r = v >= 0 ? (u64)v % q : hm::neg((u64)(-(v + 1)) % q + 1, q);
+            host[(size_t)i * K * O + e] = hm::mont(r, q);
+        }
+    }
+    u64 *d = nullptr;
+    if (cudaMalloc((void **)&d, host.size() * 8) != cudaSuccess) return fail(FHE_ENOMEM, "ct_gemm weight table");
+    CU(cudaMemcpyAsync(d, host.data(), host.size() * 8, cudaMemcpyHostToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));          // host staging goes out of scope
+    c->gemm_tabs[h] = d;
+    *tab = d;
+    return 0;
+}
+
+extern "C" int fhe_ct_gemm(fhe_ctx *c, fhe_ct *const *a, uint32_t K, const int64_t *w, uint32_t O, fhe_ct *const *out) {
+    if (K < 1 || O < 1) return fail(FHE_EINVAL, "ct_gemm: empty operand list");
+    for (u32 k = 0; k < K; k++)
+        if (!same_shape(a[k], a[0])) return fail(FHE_ELEVEL, "ct_gemm: shape/level mismatch");
+    for (u32 o = 0; o < O; o++) {
+        if (!same_shape(out[o], a[0])) return fail(FHE_ELEVEL, "ct_gemm: shape/level mismatch");
+        for (u32 k = 0; k < K; k++)
+            if (out[o]->d == a[k]->d) return fail(FHE_EINVAL, "ct_gemm: out must not alias an input");
+    }
+    const u64 *tab = nullptr;
+    TRY(gemm_table(c, w, K, O, &tab));
+    const u32 l = a[0]->level;
+    u64 maxq = 0;
+    for (u32 i = 0; i < l; i++) maxq = std::max<u64>(maxq, c->P.q[i]);
+    const int kc = (int)std::min<u64>(GEMM_MAXK, ~0ull / maxq);          // kc q < 2^64
+    const int rows = (int)(a[0]->count * 2 * l);
+    const unsigned bx = (unsigned)std::max<size_t>(1, (c->n / 2 + 255) / 256);
+    c->alg_mm += (double)rows * c->n * K * O;
+    for (u32 o0 = 0; o0 < O; o0 += GEMM_OT) {
+        const int ot = (int)std::min<u32>(GEMM_OT, O - o0);
+        for (u32 k0 = 0; k0 < K; k0 += GEMM_MAXK) {
+            const int kk = (int)std::min<u32>(GEMM_MAXK, K - k0);
+            GemmTab t;
+            memset(&t, 0, sizeof t);
+            for (int k = 0; k < kk; k++) t.in[k] = a[k0 + k]->d;
+            for (int o = 0; o < ot; o++) t.out[o] = out[o0 + o]->d;
+            ProfScope ps_(c, "k_ct_gemm");
+            if (k0 == 0)
+                k_ct_gemm<false><<<dim3(bx, rows), 256, 0, c->st>>>(t, tab, kk, (int)K, (int)k0, (int)O, (int)o0, ot, kc,
+                                                                   (int)l, (int)c->logn, c->d_mods);
+            else
+                k_ct_gemm<true><<<dim3(bx, rows), 256, 0, c->st>>>(t, tab, kk, (int)K, (int)k0, (int)O, (int)o0, ot, kc,
+                                                                  (int)l, (int)c->logn, c->d_mods);
+            CHECK_LAUNCH();
+        }
     }
     return 0;
 }

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_rot_gather_intt(PtrT
     u64 v[C::E];
     if constexpr (C::CL == 0) {
         #pragma unroll
-        for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) sm[C::pad(x)] = src[x];
+        for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) sm[C::pad(x)] = ld_stream(src + x);
         __syncthreads();
         ntt_inv_core<LOGN>(v, sm, M, tid, g);
     } else {
@@ -250,7 +250,7 @@ DEV void modup_row(const DigitTab &dt, u64 *Ext, int l, int special_id, const Mo
     u64 v[C::E];
     // centered lift: sign-symmetric, so it commutes with automorphisms (hoisted rotations)
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(src[C::io(tid, e)], half_j, qj_mod, M);
+    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(src + C::io(tid, e)), half_j, qj_mod, M);
     const int B = ntt_fwd_row<LOGN, false, FwdW5<LOGN>::value>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
     // the inner product accepts lazy digits while (l + 2) B q < 2^64 (its 128-bit sums of
@@ -331,7 +331,7 @@ DEV void rescale_row(const RescaleArgs &a, const ModInfo *__restrict__ mods, int
     const u64 *r = a.coef[s] + p * a.coef_pstride;
     u64 v[C::E];
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(r[C::io(tid, e)], half_src, msrc_q, M);
+    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(r + C::io(tid, e)), half_src, msrc_q, M);
     const int B = ntt_fwd_row<LOGN, false, RescaleW<LOGN>::value>(v, sm, M, tid);
     const u64 *base = a.base[s] + p * a.base_pstride + i * n + gb;
     u64 *out = a.out[s] + p * a.out_pstride + i * n + gb;
@@ -344,7 +344,7 @@ DEV void rescale_row(const RescaleArgs &a, const ModInfo *__restrict__ mods, int
 #pragma unroll
         for (int e = 0; e < C::E; e++) {
             const int x = tid + e * C::TH;
-            y[e] = shoup(base[x] + Bq - sm[C::pad(x)], f, fsh, M.q);
+            y[e] = shoup(ld_stream(base + x) + Bq - sm[C::pad(x)], f, fsh, M.q);
         }
     } else {
 #pragma unroll
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_ks_special(const u64
         const u32 xs = g ? galois_perm(gx, g, LOGN) : gx;
         u64 h = 0, lo = 0;
 #pragma unroll 4
-        for (int j = 0; j < l; j++) mac128(h, lo, eb[j * estride + xs], __ldg(key + j * kstride + gx));
+        for (int j = 0; j < l; j++) mac128(h, lo, ld_stream(eb + j * estride + xs), __ldg(key + j * kstride + gx));
         sm[C::pad(x)] = mont_reduce(h, lo, M.q, M.qinv);
     }
     __syncthreads();
@@ -661,6 +661,72 @@ __global__ void k_mul_scalar(const u64 *__restrict__ a, u64 *__restrict__ out, l
     GRID_STRIDE(idx, total) {
         const int i = (int)((idx >> logn) % l);
         out[idx] = shoup(a[idx], st.w[i], st.wsh[i], mods[i].q);
+    }
+}
+
+// ct-GEMM (ConvPack channel sums, reference engine.py:178-197): out[o] = sum_k w[k][o] a[k]
+// over K same-shape ciphertexts.  One polynomial row (ci, p, i) per blockIdx.y, two words per
+// thread (16-byte accesses), GEMM_OT outputs per thread: every input word is read once
+// per tile of GEMM_OT outputs and multiplied into GEMM_OT 128-bit accumulators.  The
+// weights (w mod q_i in Montgomery form, table wt[i][k][o]) of the row's prime sit in
+// shared memory.  Products accumulate lazily in 128 bits and are Montgomery-reduced every
+// kc terms (kc q_i < 2^64 keeps the sum below q_i 2^64, the reduction's bound); results
+// are canonical, hence equal to the mul_scalar / add sequence word for word.
+#define GEMM_OT 8
+#define GEMM_MAXK 64
+struct GemmTab {
+    const u64 *in[GEMM_MAXK];
+    u64 *out[GEMM_OT];
+};
+template <bool ACC>
+__global__ void __launch_bounds__(256) k_ct_gemm(const GemmTab t, const u64 *__restrict__ wt, int K, int Kall, int k0,
+                                                 int O, int o0, int ot, int kc, int l, int logn,
+                                                 const ModInfo *__restrict__ mods) {
+    __shared__ u64 wsm[GEMM_MAXK * GEMM_OT];
+    const int row = blockIdx.y, i = row % l;
+    for (int e = threadIdx.x; e < K * GEMM_OT; e += blockDim.x) {
+        const int k = e / GEMM_OT, o = e % GEMM_OT;
+        wsm[e] = o < ot ? wt[((long long)i * Kall + k0 + k) * O + o0 + o] : 0;
+    }
+    __syncthreads();
+    const long long n = 1ll << logn;
+    const long long x = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+    if (x >= n) return;
+    const ModInfo &M = mods[i];
+    const u64 q = M.q, qi = M.qinv;
+    const long long off = (long long)row * n + x;
+    u64 h0[GEMM_OT], l0[GEMM_OT], h1[GEMM_OT], l1[GEMM_OT], r0[GEMM_OT], r1[GEMM_OT];
+#pragma unroll
+    for (int o = 0; o < GEMM_OT; o++) h0[o] = l0[o] = h1[o] = l1[o] = r0[o] = r1[o] = 0;
+    int pending = 0;
+    for (int k = 0; k < K; k++) {
+        const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(t.in[k] + off);
+#pragma unroll
+        for (int o = 0; o < GEMM_OT; o++) {
+            const u64 w = wsm[k * GEMM_OT + o];
+            mac128(h0[o], l0[o], av.x, w);
+            mac128(h1[o], l1[o], av.y, w);
+        }
+        if (++pending == kc || k == K - 1) {
+#pragma unroll
+            for (int o = 0; o < GEMM_OT; o++) {
+                r0[o] = addm(r0[o], mont_reduce(h0[o], l0[o], q, qi), q);
+                r1[o] = addm(r1[o], mont_reduce(h1[o], l1[o], q, qi), q);
+                h0[o] = l0[o] = h1[o] = l1[o] = 0;
+            }
+            pending = 0;
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < GEMM_OT; o++) {
+        if (o >= ot) break;
+        u64 *dst = t.out[o] + off;
+        if (ACC) {
+            const ulonglong2 cv = *reinterpret_cast<const ulonglong2 *>(dst);
+            r0[o] = addm(r0[o], cv.x, q);
+            r1[o] = addm(r1[o], cv.y, q);
+        }
+        *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(r0[o], r1[o]);
     }
 }
 

@@ -101,19 +101,62 @@ struct DefaultWInv {   // inverse transforms
 // The twiddles of one stage for one thread are D = 2^(W - b - 1) consecutive table
 // entries starting at an even index (b: the stage's butterfly bit within the thread's
 // words); pairs of (w, w') entries are fetched with one 256-bit load.
-DEV void ldg_tw2(const ulonglong2 *p, ulonglong2 &a, ulonglong2 &b) {
+// L1 policy (NTT_L1_POLICY=1): the twiddles of the early stages (tables of at most
+// NTT_TW_KEEP_LOG entries, shared by many threads and rows) are loaded evict-last, the
+// large late-stage tables and the streamed row data no-allocate, so the rows streaming
+// through an SM do not evict the twiddles every CTA keeps re-reading.
+#ifndef NTT_L1_POLICY
+#define NTT_L1_POLICY 0
+#endif
+#ifndef NTT_TW_KEEP_LOG
+#define NTT_TW_KEEP_LOG 11
+#endif
+DEV void ldg_tw2(const ulonglong2 *p, ulonglong2 &a, ulonglong2 &b, bool keep) {
+#if NTT_L1_POLICY
+    if (keep)
+        asm("ld.global.nc.L1::evict_last.v4.u64 {%0, %1, %2, %3}, [%4];"
+            : "=l"(a.x), "=l"(a.y), "=l"(b.x), "=l"(b.y)
+            : "l"(p));
+    else
+        asm("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+            : "=l"(a.x), "=l"(a.y), "=l"(b.x), "=l"(b.y)
+            : "l"(p));
+#else
     asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
         : "=l"(a.x), "=l"(a.y), "=l"(b.x), "=l"(b.y)
         : "l"(p));
+#endif
 }
+DEV ulonglong2 ldg_tw1(const ulonglong2 *p, bool keep) {
+#if NTT_L1_POLICY
+    ulonglong2 a;
+    if (keep) asm("ld.global.nc.L1::evict_last.v2.u64 {%0, %1}, [%2];" : "=l"(a.x), "=l"(a.y) : "l"(p));
+    else asm("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(a.x), "=l"(a.y) : "l"(p));
+    return a;
+#else
+    return __ldg(p);
+#endif
+}
+// streamed row data (read once per row): no L1 allocation under the policy
+DEV u64 ld_stream(const u64 *p) {
+#if NTT_L1_POLICY
+    u64 x;
+    asm volatile("ld.global.L1::no_allocate.u64 %0, [%1];" : "=l"(x) : "l"(p));
+    return x;
+#else
+    return *p;
+#endif
+}
+// logt: log2 of the stage's twiddle-table length (the stage index)
 template <int ND>
-DEV void fetch_tw(ulonglong2 (&tw)[ND], const ulonglong2 *p, int D) {
+DEV void fetch_tw(ulonglong2 (&tw)[ND], const ulonglong2 *p, int D, int logt = 0) {
+    const bool keep = logt <= NTT_TW_KEEP_LOG;
     if (D == 1) {
-        tw[0] = __ldg(p);
+        tw[0] = ldg_tw1(p, keep);
     } else {
 #pragma unroll
         for (int d = 0; d < ND; d += 2)
-            if (d < D) ldg_tw2(p + d, tw[d], tw[d + 1]);
+            if (d < D) ldg_tw2(p + d, tw[d], tw[d + 1], keep);
     }
 }
 
@@ -169,7 +212,7 @@ DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, i
                     if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
             }
             ulonglong2 tw[E / 2];
-            fetch_tw(tw, M.tw + (1u << s) + ((u32)fidx<W>(tid, 0, f0) >> (LOGN - s)), E >> (b + 1));
+            fetch_tw(tw, M.tw + (1u << s) + ((u32)fidx<W>(tid, 0, f0) >> (LOGN - s)), E >> (b + 1), s);
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
@@ -221,7 +264,7 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
                 continue;
             }
             ulonglong2 tw[E / 2];
-            fetch_tw(tw, M.itw + (u32)h + ((u32)fidx<W>(tid, 0, f0) >> (lt + 1)), E >> (b + 1));
+            fetch_tw(tw, M.itw + (u32)h + ((u32)fidx<W>(tid, 0, f0) >> (lt + 1)), E >> (b + 1), LOGN - 1 - lt);
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
@@ -305,7 +348,7 @@ DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false, WO>::E], u64 *sm, const Mod
                 if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
         }
         ulonglong2 tw[E / 2];
-        fetch_tw(tw, M.tw + (1 << s), E >> (b + 1));
+        fetch_tw(tw, M.tw + (1 << s), E >> (b + 1), s);
 #pragma unroll
         for (int e = 0; e < E; e++) {
             if (e & (1 << b)) continue;
@@ -344,7 +387,7 @@ DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false, WO>::E], u64 *sm, const Mod
             }
             ulonglong2 tw[E / 2];
             fetch_tw(tw, M.tw + (1u << (sl + CL)) + ((u32)rank << sl) + ((u32)fidx<W>(tid, 0, f0) >> (LOGL - sl)),
-                     E >> (b + 1));
+                     E >> (b + 1), sl + CL);
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
@@ -389,7 +432,7 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
             Lz.stage();
             ulonglong2 tw[E / 2];
             fetch_tw(tw, M.itw + (u32)(N >> (lt + 1)) + ((u32)rank << (LOGL - lt - 1)) + ((u32)fidx<W>(tid, 0, f0) >> (lt + 1)),
-                     E >> (b + 1));
+                     E >> (b + 1), LOGN - 1 - lt);
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
@@ -425,7 +468,7 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
             continue;
         }
         ulonglong2 tw[E / 2];
-        fetch_tw(tw, M.itw + (N >> (lt + 1)), E >> (b + 1));
+        fetch_tw(tw, M.itw + (N >> (lt + 1)), E >> (b + 1), LOGN - 1 - lt);
 #pragma unroll
         for (int e = 0; e < E; e++) {
             if (e & (1 << b)) continue;

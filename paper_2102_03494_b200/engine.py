@@ -287,6 +287,11 @@ def conv_conv(x: ConvPacked, w: WeightMatrix, ctx):
     if w.k != x.k:
         raise ValueError(f"weight matrix has {w.k} rows but input has {x.k} columns")
     before = ctx.counters.copy()
+    if hasattr(ctx, "ct_gemm"):
+        # one ct-GEMM pass: every column is read once per tile of outputs (fhe_ct_gemm)
+        outs = ctx.ct_gemm(list(x.cts), [[int(w.entries[k, o]) for o in range(w.out_channels)] for k in range(x.k)])
+        if outs is not None:
+            return ChannelPacked(tuple(outs), x.spatial), [_phase(ctx, "channel-sums", before)]
     chans = []
     for o in range(w.out_channels):
         terms = [_scalar_term(ctx, x, k, int(w.entries[k, o])) for k in range(x.k)]

@@ -707,10 +707,78 @@ class HeContext:
             if self.debug_checks and tracked:
                 self.check()                       # immediate, like the reference (hesim.py:360-361)
         rounds = (m - 1).bit_length()
-        acc = cts
-        for h in reversed(range(rounds)):
-            acc = self._rotate_add_many(acc, 1 << h)
-        return acc
+        if rounds == 0:
+            return cts
+        # ceil(log2 m) rotations and additions per ciphertext (hesim.py:363-365); the device
+        # runs every level as one fused launch sequence inside one call (fhe_rotate_and_sum)
+        self.counters.rot += rounds * len(cts)
+        self.counters.add_cc += rounds * len(cts)
+        self.rotation_steps.update(1 << h for h in range(rounds))
+        if not cts[0].tracked:
+            return [SlotCiphertext(None, c.depth, c.params, c.assembly_depth) for c in cts]
+        groups: dict[int, list[int]] = {}
+        for i, c in enumerate(cts):
+            groups.setdefault(c.handle.level, []).append(i)
+        outs = [None] * len(cts)
+        for idx in groups.values():
+            res = self.evaluator.rotate_and_sum([cts[i].handle for i in idx], m)
+            for i, h in zip(idx, res):
+                outs[i] = self._wrap(h, cts[i].depth, cts[i].assembly_depth)
+        return outs
+
+    def combine(self, cts, lengths):
+        """Concatenate slot-0-anchored payloads as a pairwise tree in one device call
+        (fhe_combine; packing.tree_combine states the schedule): len - 1 rotations and
+        additions, as the reference's chain (packing.py:350-368).  Returns None when the
+        operands cannot go down in one call (mixed levels or tracking)."""
+        cts, lengths = list(cts), [int(v) for v in lengths]
+        n = self.params.n_slots
+        if len(cts) < 2 or any(v < 1 for v in lengths) or sum(lengths) > n:
+            return None
+        tracked = [c.tracked for c in cts]
+        if any(tracked) != all(tracked):
+            return None
+        if tracked[0] and len({c.handle.level for c in cts}) != 1:
+            return None
+        lens, steps = lengths, []
+        while len(lens) > 1:
+            nxt = []
+            for k in range(0, len(lens) - 1, 2):
+                steps.append(n - lens[k])
+                nxt.append(lens[k] + lens[k + 1])
+            if len(lens) % 2:
+                nxt.append(lens[-1])
+            lens = nxt
+        self.counters.rot += len(steps)
+        self.counters.add_cc += len(steps)
+        self.rotation_steps.update(steps)
+        depth = max(c.depth for c in cts)
+        adepth = max(c.assembly_depth for c in cts)
+        if not tracked[0]:
+            return SlotCiphertext(None, depth, cts[0].params, adepth)
+        return self._wrap(self.evaluator.combine([c.handle for c in cts], lengths), depth, adepth)
+
+    def ct_gemm(self, cts, w):
+        """out[o] = sum_k w[k][o] * cts[k] in one device pass (fhe_ct_gemm): the ConvPack
+        channel sums of engine.py:178-197, tallied as the reference tallies them --
+        O*K constant multiplies and O*(K-1) additions.  Valid where mul_scalar is (every
+        slot outside the constants' support is zero).  Returns None when the operands
+        cannot go down in one call."""
+        cts = list(cts)
+        K, O = len(cts), len(w[0])
+        tracked = [c.tracked for c in cts]
+        if any(tracked) != all(tracked):
+            return None
+        if tracked[0] and len({c.handle.level for c in cts}) != 1:
+            return None
+        self.counters.mul_pc += O * K
+        self.counters.add_cc += O * (K - 1)
+        depth = max(c.depth for c in cts) + 1
+        adepth = max(c.assembly_depth for c in cts)
+        if not tracked[0]:
+            return [SlotCiphertext(None, depth, cts[0].params, adepth) for _ in range(O)]
+        outs = self.evaluator.ct_gemm([c.handle for c in cts], w)
+        return [self._wrap(o, depth, adepth) for o in outs]
 
     def _rotate_add_many(self, cts, k: int):
         """acc + rotate(acc, k) for every acc: one rotation and one addition each

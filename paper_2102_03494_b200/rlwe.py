@@ -305,6 +305,31 @@ class Evaluator:
                       len(a))
         return outs
 
+    def rotate_and_sum(self, cts, span: int) -> list[Ciphertext]:
+        """slot 0 of out[i] <- sum of the first `span` slots of cts[i]; every tree level is
+        one fused rotate-and-add launch sequence over all objects (fhe_rotate_and_sum)."""
+        outs = [self.new_ct(c.rows, c.level) for c in cts]
+        self.lib.call("fhe_rotate_and_sum", self.ctx, handle_array([c.ptr for c in cts]),
+                      handle_array([o.ptr for o in outs]), len(cts), int(span))
+        return outs
+
+    def combine(self, cts, lengths) -> Ciphertext:
+        """Tree concatenation of slot-0-anchored payloads (fhe_combine)."""
+        out = self.new_ct(cts[0].rows, cts[0].level)
+        arr = (ctypes.c_uint32 * len(lengths))(*[int(v) for v in lengths])
+        self.lib.call("fhe_combine", self.ctx, handle_array([c.ptr for c in cts]), arr, len(cts), out.ptr)
+        return out
+
+    def ct_gemm(self, cts, w) -> list[Ciphertext]:
+        """out[o] = sum_k w[k][o] * cts[k] (fhe_ct_gemm); w is a K x O integer matrix."""
+        K, O = len(cts), len(w[0])
+        flat = [int(w[k][o]) for k in range(K) for o in range(O)]
+        arr = (ctypes.c_int64 * len(flat))(*flat)
+        outs = [self.new_ct(cts[0].rows, cts[0].level) for _ in range(O)]
+        self.lib.call("fhe_ct_gemm", self.ctx, handle_array([c.ptr for c in cts]), K, arr, O,
+                      handle_array([o.ptr for o in outs]))
+        return outs
+
     def copy(self, src: Ciphertext, dst: Ciphertext) -> None:
         """dst <- src words on the device (same rows and level), asynchronous."""
         self.lib.call("fhe_ct_copy", self.ctx, src.ptr, dst.ptr)

@@ -60,3 +60,73 @@ def test_empty_batches_golden(golden_lib):
     assert ev.rotate_hoisted(ct, []) == []
     assert ev.mul_plain_many([], []) == []
     assert ev.add_many([], []) == []
+
+
+def _slots(P, R, rng, bound=None):
+    return np.stack([rng.integers(0, bound or ti, size=(R, P.n), dtype=np.uint64) for ti in P.t]).astype(np.uint64)
+
+
+def test_composite_operators_equal_their_sequences(golden_lib):
+    """fhe_rotate_and_sum / fhe_combine / fhe_ct_gemm are the reference's rotate_and_sum
+    (hesim.py:347-366), combine_to_dense (packing.py:350-368) and conv_conv channel sums
+    (engine.py:178-197): their words equal the primitive sequences and their slots the
+    reference semantics."""
+    P = make_params(64, [65537], levels=3, q_bits=50)
+    ev = Evaluator(P, golden_lib)
+    N, t = P.n_slots, 65537
+    rng = np.random.default_rng(4)
+    # rotate_and_sum over a 37-slot payload (zero tail): slot 0 = sum of the payload
+    s = np.zeros((1, 2, P.n), dtype=np.uint64)
+    s[0, :, :37] = rng.integers(0, t, size=(2, 37))
+    s[0, 1, N:N + 37] = rng.integers(0, t, size=37)
+    a = ev.encrypt(s)
+    out = ev.rotate_and_sum([a], 37)[0]
+    acc = a
+    for h in reversed(range(6)):
+        acc = ev.add(acc, ev.rotate(acc, 1 << h))
+    assert np.array_equal(ev.read(out), ev.read(acc))
+    dec = ev.decrypt(out)
+    assert int(dec[0, 0, 0]) == int(s[0, 0, :37].astype(object).sum() % t)
+    assert int(dec[0, 1, N]) == int(s[0, 1, N:N + 37].astype(object).sum() % t)
+    assert np.array_equal(ev.read(ev.rotate_and_sum([a], 1)[0]), ev.read(a))
+    # combine: unequal lengths, odd count
+    lengths = [5, 3, 7, 2, 4]
+    payloads, cts = [], []
+    for ln in lengths:
+        v = np.zeros((1, 1, P.n), dtype=np.uint64)
+        v[0, 0, :ln] = rng.integers(1, t, size=ln)
+        v[0, 0, N:N + ln] = rng.integers(1, t, size=ln)
+        payloads.append(v)
+        cts.append(ev.encrypt(v))
+    comb = ev.decrypt(ev.combine(cts, lengths))
+    off = 0
+    for v, ln in zip(payloads, lengths):
+        assert np.array_equal(comb[0, 0, off:off + ln], v[0, 0, :ln])
+        assert np.array_equal(comb[0, 0, N + off:N + off + ln], v[0, 0, N:N + ln])
+        off += ln
+    assert not comb[0, 0, off:N].any()
+    assert np.array_equal(ev.read(ev.combine(cts[:1], lengths[:1])), ev.read(cts[0]))
+    # ct_gemm: K = 3 inputs, O = 10 outputs (two output tiles), signed weights
+    ins = [_slots(P, 2, rng) for _ in range(3)]
+    cin = [ev.encrypt(x) for x in ins]
+    w = rng.integers(-127, 128, size=(3, 10))
+    outs = ev.ct_gemm(cin, w.tolist())
+    for o, co in enumerate(outs):
+        seq = ev.mul_scalar(cin[0], int(w[0, o]))
+        for k in (1, 2):
+            seq = ev.add(seq, ev.mul_scalar(cin[k], int(w[k, o])))
+        assert np.array_equal(ev.read(co), ev.read(seq))
+        want = sum(ins[k].astype(object) * int(w[k, o]) for k in range(3)) % t
+        assert np.array_equal(ev.decrypt(co).astype(object), want)
+
+
+def test_composite_operator_errors(golden_lib):
+    P = make_params(8, [97], levels=2, q_bits=40)
+    ev = Evaluator(P, golden_lib)
+    a = ev.encrypt(np.zeros((1, 1, 16), dtype=np.uint64))
+    with pytest.raises(FheError):
+        ev.rotate_and_sum([a], 9)                  # span > N
+    with pytest.raises(FheError):
+        ev.combine([a, a], [5, 4])                 # 9 slots > N = 8
+    with pytest.raises(FheError):
+        ev.combine([a, a], [0, 4])                 # empty payload

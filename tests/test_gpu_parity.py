@@ -267,3 +267,61 @@ def test_empty_batches(golden_lib, cuda_lib):
         assert ev.rotate_hoisted(ct, []) == []
         assert ev.mul_plain_many([], []) == []
         assert ev.add_many([], []) == []
+
+
+COMPOSITE_CASES = [CASES[1], CASES[2], CASES[4], CASES[6], CASES[7], CASES[-2]]
+
+
+@pytest.mark.parametrize("case", COMPOSITE_CASES, ids=lambda c: f"N{c[0]}-T{len(c[1])}-L{c[2]}-q{c[3]}")
+def test_composite_operators_bit_exact(case, golden_lib, cuda_lib):
+    """fhe_rotate_and_sum, fhe_combine and fhe_ct_gemm: GPU words equal the
+    golden model's, which equal the reference sequences (tests/test_golden_model.py)."""
+    gd, gp, P = _pair(case, golden_lib, cuda_lib)
+    rng = np.random.default_rng(11)
+    N = P.n_slots
+
+    def mirror(slots, nonce):
+        g = gd.encrypt(slots, nonce=nonce)
+        c = gp.new_ct(slots.shape[1])
+        gp.write(c, gd.read(g))
+        return g, c
+
+    # rotate_and_sum over several objects with different row counts, span not a power of two
+    span = max(2, min(N, 37))
+    objs = [mirror(_rand_slots(P, 1 + i % 2, rng), 20 + i) for i in range(3)]
+    for og, oc in zip(gd.rotate_and_sum([g for g, _ in objs], span), gp.rotate_and_sum([c for _, c in objs], span)):
+        assert np.array_equal(gd.read(og), gp.read(oc))
+    og, oc = gd.rotate_and_sum([objs[0][0]], 1)[0], gp.rotate_and_sum([objs[0][1]], 1)[0]
+    assert np.array_equal(gd.read(og), gp.read(oc))
+    # combine: unequal lengths, odd count (a block that moves up a level unchanged)
+    lengths = [max(1, N // 16), max(1, N // 32), max(1, N // 8), 1, max(1, N // 16)]
+    if sum(lengths) > N:
+        lengths = [1, 1, 1]
+    blocks = [mirror(_rand_slots(P, 2, rng), 40 + i) for i in range(len(lengths))]
+    assert np.array_equal(gd.read(gd.combine([g for g, _ in blocks], lengths)),
+                          gp.read(gp.combine([c for _, c in blocks], lengths)))
+    assert np.array_equal(gd.read(gd.combine([blocks[0][0]], lengths[:1])), gp.read(gp.combine([blocks[0][1]], lengths[:1])))
+    # ct_gemm: K = 11 inputs (more than one lazy-accumulation chunk at 61 bits), O = 10 (two tiles)
+    K, O = 11, 10
+    ins = [mirror(_rand_slots(P, 2, rng), 60 + k) for k in range(K)]
+    w = rng.integers(-127, 128, size=(K, O))
+    w[0, 0] = -(1 << 62)                              # full-range int64 weights reduce per prime
+    for og, oc in zip(gd.ct_gemm([g for g, _ in ins], w.tolist()), gp.ct_gemm([c for _, c in ins], w.tolist())):
+        assert np.array_equal(gd.read(og), gp.read(oc))
+
+
+def test_ct_gemm_wide_k_on_gpu(golden_lib, cuda_lib):
+    """More inputs than one launch's pointer table (GEMM_MAXK = 64): chained accumulating launches."""
+    gd, gp, P = _pair(CASES[1], golden_lib, cuda_lib)
+    rng = np.random.default_rng(12)
+    K, O = 70, 3
+    base = [_rand_slots(P, 1, rng) for _ in range(K)]
+    gi = [gd.encrypt(s, nonce=100 + k) for k, s in enumerate(base)]
+    ci = []
+    for g in gi:
+        c = gp.new_ct(1)
+        gp.write(c, gd.read(g))
+        ci.append(c)
+    w = rng.integers(-(1 << 40), 1 << 40, size=(K, O))
+    for og, oc in zip(gd.ct_gemm(gi, w.tolist()), gp.ct_gemm(ci, w.tolist())):
+        assert np.array_equal(gd.read(og), gp.read(oc))
