@@ -117,6 +117,18 @@ DEV u64 centered_lift_lazy(u64 x, u64 half_src, u64 msrc_q, const ModInfo &M) {
     const u64 r = x + mulhi_approx(x, M.mu) * M.nq;
     return x > half_src ? r + (M.q - msrc_q) : r;
 }
+// The same lift without any multiplication, for source moduli below 8q: a centered value
+// lies in [-half_src, half_src], so when half_src < 4q the non-negative ones already are
+// representatives below 4q (the forward NTT's input bound) and the negative ones become so
+// after adding k q, k = ceil(half_src / q) <= 4.  lift_offset returns k q - m_src (mod
+// 2^64), or 0 when the source modulus is too large and the Barrett form must be used
+// (0 is never a valid offset: k q = m_src has no solution for distinct primes).
+DEV u64 lift_offset(u64 half_src, u64 m_src, u64 q) {
+    if (half_src >= 4 * q) return 0;
+    const u64 k = 1 + (half_src > q) + (half_src > 2 * q) + (half_src > 3 * q);
+    return k * q - m_src;
+}
+DEV u64 centered_lift_add(u64 x, u64 half_src, u64 off) { return x > half_src ? x + off : x; }
 // x mod q, lazily in [0, 3q), any 64-bit x
 DEV u64 red_lazy(u64 x, const ModInfo &M) { return x + mulhi_approx(x, M.mu) * M.nq; }
 // x (128-bit) mod q

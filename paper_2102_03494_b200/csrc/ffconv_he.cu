@@ -601,13 +601,15 @@ static int setup_secret(fhe_ctx *c) {
 static int setup_workspace(fhe_ctx *c) {
     size_t n = c->n, L = c->L;
     size_t per_ct = n * (L + L * (L + 1) + 2 * (L + 1)) * 8;
-    size_t budget = 512ull << 20;
+    // sub-batch: as many ciphertexts as 1.25 GB of workspace per lane holds, at most MAXS
+    // (128 measured best at configs[1]: fewer partial waves of the row kernels;
+    // profiles/r02_subbatch.json)
+    size_t budget = 1280ull << 20;
     const char *env = getenv("FHE_KS_BATCH");
     int S = env ? atoi(env) : (int)(budget / per_ct);
     if (!env && S < 8) S = 8;          // large rings: keep >= 8 ciphertexts per sub-batch
     if (S < 1) S = 1;
     if (S > MAXS) S = MAXS;
-    if (!env && S > 64) S = 64;        // default sub-batch (FHE_KS_BATCH up to MAXS)
     c->S = S;
     const char *lenv = getenv("FHE_LANES");
     c->lanes = lenv ? std::max(1, std::min(fhe_ctx::MAXLANES, atoi(lenv))) : 2;

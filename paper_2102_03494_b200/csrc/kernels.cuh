@@ -249,8 +249,15 @@ DEV void modup_row(const DigitTab &dt, u64 *Ext, int l, int special_id, const Mo
     const u64 *src = dt.coef[s] + j * n;
     u64 v[C::E];
     // centered lift: sign-symmetric, so it commutes with automorphisms (hoisted rotations)
+    // source digits below 8 q_i lift with a compare and an add (arith.cuh lift_offset)
+    const u64 off = lift_offset(half_j, Sj.q, M.q);
+    if (off) {
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(src + C::io(tid, e)), half_j, qj_mod, M);
+        for (int e = 0; e < C::E; e++) v[e] = centered_lift_add(ld_stream(src + C::io(tid, e)), half_j, off);
+    } else {
+#pragma unroll
+        for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(src + C::io(tid, e)), half_j, qj_mod, M);
+    }
     const int B = ntt_fwd_row<LOGN, false, FwdW5<LOGN>::value>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
     // the inner product accepts lazy digits while (l + 2) B q < 2^64 (its 128-bit sums of
@@ -330,8 +337,14 @@ DEV void rescale_row(const RescaleArgs &a, const ModInfo *__restrict__ mods, int
     const u64 half_src = S.half, msrc_q = red64(S.q, M.q, M.mu);
     const u64 *r = a.coef[s] + p * a.coef_pstride;
     u64 v[C::E];
+    const u64 off = lift_offset(half_src, S.q, M.q);
+    if (off) {
 #pragma unroll
-    for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(r + C::io(tid, e)), half_src, msrc_q, M);
+        for (int e = 0; e < C::E; e++) v[e] = centered_lift_add(ld_stream(r + C::io(tid, e)), half_src, off);
+    } else {
+#pragma unroll
+        for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(r + C::io(tid, e)), half_src, msrc_q, M);
+    }
     const int B = ntt_fwd_row<LOGN, false, RescaleW<LOGN>::value>(v, sm, M, tid);
     const u64 *base = a.base[s] + p * a.base_pstride + i * n + gb;
     u64 *out = a.out[s] + p * a.out_pstride + i * n + gb;

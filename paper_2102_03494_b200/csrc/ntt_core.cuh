@@ -106,7 +106,7 @@ struct DefaultWInv {   // inverse transforms
 // large late-stage tables and the streamed row data no-allocate, so the rows streaming
 // through an SM do not evict the twiddles every CTA keeps re-reading.
 #ifndef NTT_L1_POLICY
-#define NTT_L1_POLICY 0
+#define NTT_L1_POLICY 1
 #endif
 #ifndef NTT_TW_KEEP_LOG
 #define NTT_TW_KEEP_LOG 11

@@ -33,33 +33,33 @@ def t(label, fn, reps=5):
 ct = ev.encrypt(pin_in)
 ev.sync()
 t("encrypt pageable", lambda: ev.encrypt(slots))
-t("encrypt pinned (async)", lambda: ev.encrypt(pin_in))
+t("encrypt pinned (async)", lambda: ev.encrypt(pin_in, async_=True))
 t("rotate", lambda: ev.rotate(ct, k))
 t("decrypt pageable", lambda: ev.decrypt(ct))
-t("decrypt pinned (async)", lambda: ev.decrypt(ct, out=pin_out))
+t("decrypt pinned (async)", lambda: ev.decrypt(ct, out=pin_out, async_=True))
 for ch in (1, 4, 8, 16):
     bounds = [(B * i // ch, B * (i + 1) // ch) for i in range(ch)]
 
     def step():
         for r0, r1 in bounds:
-            c = ev.encrypt(pin_in[:, r0:r1])
+            c = ev.encrypt(pin_in[:, r0:r1], async_=True)
             r = ev.rotate(c, k)
-            ev.decrypt(r, out=pin_out[:, r0:r1])
+            ev.decrypt(r, out=pin_out[:, r0:r1], async_=True)
     t(f"e2e chunks={ch}", step)
 for ch in (8,):
     bounds = [(B * i // ch, B * (i + 1) // ch) for i in range(ch)]
 
     def step2():
-        cs = [ev.encrypt(pin_in[:, r0:r1]) for r0, r1 in bounds]
+        cs = [ev.encrypt(pin_in[:, r0:r1], async_=True) for r0, r1 in bounds]
         rs = ev.rotate_many(cs, k)
         for (r0, r1), r in zip(bounds, rs):
-            ev.decrypt(r, out=pin_out[:, r0:r1])
+            ev.decrypt(r, out=pin_out[:, r0:r1], async_=True)
     t(f"e2e enc/dec chunks={ch} + rotate_many", step2)
 
 # per-kernel breakdown of encrypt / decrypt (single stream, isolated kernel times)
 import ctypes  # noqa: E402
 lib = ev.lib
-for label, fn in (("encrypt", lambda: ev.encrypt(pin_in)), ("decrypt", lambda: ev.decrypt(ct, out=pin_out))):
+for label, fn in (("encrypt", lambda: ev.encrypt(pin_in, async_=True)), ("decrypt", lambda: ev.decrypt(ct, out=pin_out, async_=True))):
     fn(); ev.sync()
     lib.call("fhe_prof_enable", ev.ctx, 1)
     fn(); ev.sync()
