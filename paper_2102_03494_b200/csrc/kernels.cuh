@@ -258,8 +258,20 @@ DEV void modup_row(const DigitTab &dt, u64 *Ext, int l, int special_id, const Mo
 #pragma unroll
         for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(src + C::io(tid, e)), half_j, qj_mod, M);
     }
-    const int B = ntt_fwd_row<LOGN, false, FwdW5<LOGN>::value>(v, sm, M, tid);
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
+    if constexpr (C::CL == 0 && LOGN >= 5) {
+        // single-CTA rows: the last pass's results go from the registers straight to global
+        // memory (32 consecutive words per thread, 32-byte stores): no staging pass, and the
+        // shared memory is free for the next row without another barrier
+        const int B = ntt_fwd_core<LOGN, C::W, false, true>(v, sm, M, tid);
+        if (!((u128)(l + 2) * (u64)B * M.q < ((u128)1 << 64))) {
+#pragma unroll
+            for (int e = 0; e < C::E; e++) v[e] = red_any(v[e], M.q, M.mu, M.nq);
+        }
+        store_keep<C::E>(dst + ((long long)tid << C::W), v);
+        return;
+    }
+    const int B = ntt_fwd_row<LOGN, false, FwdW5<LOGN>::value>(v, sm, M, tid);
     // the inner product accepts lazy digits while (l + 2) B q < 2^64 (its 128-bit sums of
     // l digit terms and up to two addend terms stay below q 2^64, the Montgomery bound)
     if ((u128)(l + 2) * (u64)B * M.q < ((u128)1 << 64)) {
@@ -298,7 +310,9 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nsrc), "r"((u32)(C::N * 8)) : "memory");
         }
         modup_row<LOGN>(dt, Ext, l, special_id, mods, s, j, i, sm, tid);
-        __syncthreads();          // the next row's NTT reuses the shared memory
+        // no barrier: the row's last shared-memory reads are fenced inside the NTT core (its
+        // results leave from the registers), so warps run ahead into the next row's loads
+        if constexpr (LOGN < 5) __syncthreads();
     }
 }
 
@@ -345,11 +359,55 @@ DEV void rescale_row(const RescaleArgs &a, const ModInfo *__restrict__ mods, int
 #pragma unroll
         for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(r + C::io(tid, e)), half_src, msrc_q, M);
     }
+    const u64 *add = ((a.add_pmask >> p) & 1) && a.add[s] ? a.add[s] + p * a.add_pstride + i * n : nullptr;
+    const u64 f = a.fac[i], fsh = a.fac_sh[i];
+    if constexpr (C::CL == 0 && LOGN >= 5) {
+        // single-CTA rows: the NTT's last pass stays in the registers (E consecutive words
+        // per thread) and the epilogue runs on them with 32-byte global accesses
+        const int B = ntt_fwd_core<LOGN, C::W, false, true>(v, sm, M, tid);
+        const long long o = (long long)tid << C::W;
+        const bool lazy = (u128)(B + 1) * M.q < ((u128)1 << 64);
+        const u64 Bq = (u64)B * M.q;
+        const u32 ag = a.add_g[s];
+        if (add && ag) {
+            // the addend row staged in shared memory (free since the core's last barrier) and
+            // read through the automorphism
+#pragma unroll
+            for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) sm[C::pad(x)] = add[x];
+            __syncthreads();
+        }
+        const u64 *base = a.base[s] + p * a.base_pstride + i * n + o;
+        const u64 *acc = a.acc[s] ? a.acc[s] + p * a.acc_pstride + i * n + o : nullptr;
+        u64 *out = a.out[s] + p * a.out_pstride + i * n + o;
+        // four words at a time (32-byte accesses) to stay inside the register budget
+#pragma unroll
+        for (int e = 0; e < C::E; e += 4) {
+            u64 y[4], t[4];
+            load_keep<4>(y, base + e);
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                y[u] = lazy ? shoup(y[u] + Bq - v[e + u], f, fsh, M.q)
+                            : shoup(subm(y[u], red_any(v[e + u], M.q, M.mu, M.nq), M.q), f, fsh, M.q);
+            if (add && ag) {
+#pragma unroll
+                for (int u = 0; u < 4; u++) y[u] = addm(y[u], sm[C::pad(galois_perm((u32)o + e + u, ag, LOGN))], M.q);
+            } else if (add) {
+                load_keep<4>(t, add + o + e);
+#pragma unroll
+                for (int u = 0; u < 4; u++) y[u] = addm(y[u], t[u], M.q);
+            }
+            if (acc) {
+                load_keep<4>(t, acc + e);
+#pragma unroll
+                for (int u = 0; u < 4; u++) y[u] = addm(y[u], t[u], M.q);
+            }
+            store_keep<4>(out + e, y);
+        }
+        return;
+    }
     const int B = ntt_fwd_row<LOGN, false, RescaleW<LOGN>::value>(v, sm, M, tid);
     const u64 *base = a.base[s] + p * a.base_pstride + i * n + gb;
     u64 *out = a.out[s] + p * a.out_pstride + i * n + gb;
-    const u64 *add = ((a.add_pmask >> p) & 1) && a.add[s] ? a.add[s] + p * a.add_pstride + i * n : nullptr;
-    const u64 f = a.fac[i], fsh = a.fac_sh[i];
     u64 y[C::E];
     if ((u128)(B + 1) * M.q < ((u128)1 << 64)) {
         // lazy NTT outputs x < B q: base - x == base + B q - x (mod q), non-negative, < 2^64

@@ -186,7 +186,11 @@ DEV int fidx(int tid, int e, int f0) {
 // with __syncthreads().
 // CANON = false: the outputs are left lazy; the return value is their bound in
 // units of q (every output < bound * q <= 2^64), for callers that absorb it.
-template <int LOGN, int WW = DefaultW<LOGN>::value, bool CANON = true>
+// KEEP = true: the last pass leaves its results in the registers instead of shared memory
+// (no final store and barrier): v[e] = out[(tid << W) | e], E consecutive words per thread,
+// for callers that store or post-process them from there (store_keep / load_keep below).
+// Shared memory is then free for the next row as soon as this call returns.
+template <int LOGN, int WW = DefaultW<LOGN>::value, bool CANON = true, bool KEEP = false>
 DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid) {
     using C = NttCfg<LOGN, WW>;
     constexpr int W = C::W, E = C::E, NP = C::NP;
@@ -223,11 +227,40 @@ DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, i
 #pragma unroll
             for (int e = 0; e < E; e++) v[e] = red_any(v[e], M.q, M.mu, M.nq);
         }
+        if (KEEP && p == NP - 1) break;
 #pragma unroll
         for (int e = 0; e < E; e++) sm[C::pad(fidx<W>(tid, e, f0))] = v[e];
         __syncthreads();
     }
     return CANON ? 1 : Lz.B;
+}
+// E consecutive words of one thread to / from global memory with 32-byte accesses
+// (p 32-byte aligned for E >= 4)
+template <int E>
+DEV void store_keep(u64 *p, const u64 (&v)[E]) {
+    if constexpr (E % 4 == 0) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4)
+            asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p + e), "l"(v[e]), "l"(v[e + 1]), "l"(v[e + 2]),
+                         "l"(v[e + 3])
+                         : "memory");
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; e++) p[e] = v[e];
+    }
+}
+template <int E>
+DEV void load_keep(u64 (&v)[E], const u64 *p) {
+    if constexpr (E % 4 == 0) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4)
+            asm volatile("ld.global.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+                         : "=l"(v[e]), "=l"(v[e + 1]), "=l"(v[e + 2]), "=l"(v[e + 3])
+                         : "l"(p + e));
+    } else {
+#pragma unroll
+        for (int e = 0; e < E; e++) v[e] = p[e];
+    }
 }
 
 // Inverse. In: canonical (or < 2q) values in sm[C::pad(i)], bit-reversed order, synced.

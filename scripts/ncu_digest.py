@@ -62,6 +62,39 @@ def main(rep, out, top=60):
         f.write("\n=== SASS opcode mix (executed warp instructions, share of stall samples) ===\n")
         for op, e in ops.most_common(25):
             f.write(f"{op:12s} exec {100 * e / tot_e:5.1f}%  stalls {100 * ops_s[op] / tot_s:5.1f}%\n")
+        # per-reason stall columns of the source page (when the SourceCounters section has them)
+        reasons = [k for k in (hdr or []) if k.lower().startswith("stall_") or k.startswith("Warp Stall Sampling (")]
+        f.write("\n=== source-page columns ===\n" + " | ".join(hdr or []) + "\n")
+        def num(d, k):
+            try:
+                return float(d.get(k, "0") or 0)
+            except ValueError:
+                return 0.0
+        if reasons:
+            f.write("\n=== stall reasons over the kernel (share of samples) ===\n")
+            tot = {k: sum(num(d, k) for d in data) for k in reasons}
+            for k, v in sorted(tot.items(), key=lambda kv: -kv[1])[:14]:
+                f.write(f"{k:50s} {100 * v / tot_s:6.2f}%\n")
+        # code regions delimited by barriers: where the samples sit (load / pass / exchange phases)
+        f.write("\n=== regions between barriers (instruction index range, executed share, stall share, top reasons) ===\n")
+        start = 0
+        def flush(a, b, label):
+            seg = data[a:b]
+            if not seg:
+                return
+            e = sum(d["_e"] for d in seg)
+            st = sum(d["_s"] for d in seg)
+            top3 = ""
+            if reasons:
+                rs = sorted(((sum(num(d, k) for d in seg), k) for k in reasons if not k.endswith("(All Samples)")), reverse=True)[:3]
+                top3 = ", ".join(f"{k.replace('stall_', '')} {100 * v / max(st, 1):.0f}%" for v, k in rs)
+            mem = sum(1 for d in seg if any(t in d["Source"] for t in ("LDG", "STG")))
+            f.write(f"[{a:5d},{b:5d}) exec {100 * e / tot_e:5.1f}%  stalls {100 * st / tot_s:5.1f}%  ldg/stg {mem:3d}  {label}  {top3}\n")
+        for idx, d in enumerate(data):
+            if "BAR" in d["Source"] or "EXIT" in d["Source"]:
+                flush(start, idx + 1, d["Source"].strip()[:28])
+                start = idx + 1
+        flush(start, len(data), "end")
         f.write(f"\n=== top {top} SASS lines by stall samples (of {tot_s}) ===\n")
         for d in sorted(data, key=lambda d: -d["_s"])[:top]:
             f.write(f"{100 * d['_s'] / tot_s:5.2f}%  exec {d['_e']:>10d}  {d['Address'][-5:]}  {d['Source'].strip()[:90]}\n")
