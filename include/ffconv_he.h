@@ -175,6 +175,18 @@ int fhe_status(fhe_ctx *ctx, uint32_t *noise_dist, uint32_t *flags, int reset);
  * (the caller derives the exact invariant noise |[t x]_Q| / Q from it) */
 int fhe_decrypt_raw(fhe_ctx *ctx, const fhe_ct *ct, uint64_t *coef);
 
+/* test access to the stages of one key-switched rotation (parity after every kernel, not
+ * only after every primitive).  For each physical ciphertext of a (at most 128):
+ *   digits [count][l][n]        INTT_i(tau_g(c1)_i), the coefficient-form digits (rotation step 1)
+ *   ext    [count][l][l+1][n]   NTT_i(centered lift of digit j), canonical; column l is the
+ *                               special prime; the diagonal i == j (read from the input, never
+ *                               materialized) is zero
+ *   acc    [count][2][l+1][n]   sum_j ext_j,i * ksk_j,i per output polynomial, WITHOUT the
+ *                               rotation's c0 addend; the special prime's row (index l) in
+ *                               coefficient form, as ModDown consumes it
+ * Host pointers; the golden model and the CUDA library fill them from their own pipelines. */
+int fhe_debug_rotate_stages(fhe_ctx *ctx, const fhe_ct *a, uint32_t k, uint64_t *digits, uint64_t *ext, uint64_t *acc);
+
 /* ---- evaluation (out may alias an input unless stated) --------------------- */
 int fhe_add(fhe_ctx *ctx, const fhe_ct *a, const fhe_ct *b, fhe_ct *out);
 int fhe_mul_plain(fhe_ctx *ctx, const fhe_ct *a, const fhe_pt *pt, fhe_ct *out);

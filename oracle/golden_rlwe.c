@@ -1258,3 +1258,51 @@ int fhe_ct_gemm(fhe_ctx *c, fhe_ct *const *a, uint32_t K, const int64_t *w, uint
                 }
     return 0;
 }
+
+/* stages of one rotation's key switch (include/ffconv_he.h: fhe_debug_rotate_stages) */
+int fhe_debug_rotate_stages(fhe_ctx *c, const fhe_ct *a, uint32_t k, uint64_t *digits, uint64_t *ext, uint64_t *accout) {
+    if (k == 0 || k >= c->N) return fail(FHE_EINVAL, "rotation step %u outside [1, %u)", k, c->N);
+    u32 n = c->n, l = a->level, L = c->L;
+    u32 g = galois_elt(c, k);
+    key_node *key = get_key(c, g);
+    u64 *c1r = (u64 *)malloc((size_t)l * n * 8);
+    for (u32 ci = 0; ci < a->count; ci++) {
+        u64 *dig = digits + (size_t)ci * l * n;
+        u64 *ex = ext + (size_t)ci * l * (l + 1) * n;
+        u64 *acc = accout + (size_t)ci * 2 * (l + 1) * n;
+        memset(ex, 0, (size_t)l * (l + 1) * n * 8);
+        memset(acc, 0, (size_t)2 * (l + 1) * n * 8);
+        for (u32 i = 0; i < l; i++) {
+            automorph(c, poly(a, ci, 1, i), c1r + (size_t)i * n, g);
+            memcpy(dig + (size_t)i * n, c1r + (size_t)i * n, n * 8);
+            intt(dig + (size_t)i * n, &c->M[i], n);
+        }
+        for (u32 ii = 0; ii <= l; ii++) {
+            u32 pi = ii == l ? L : ii;
+            u64 q = modof(c, pi);
+            u64 *a0 = acc + (size_t)(0 * (l + 1) + ii) * n, *a1 = acc + (size_t)(1 * (l + 1) + ii) * n;
+            for (u32 j = 0; j < l; j++) {
+                const u64 *e;
+                if (ii == j) {
+                    e = c1r + (size_t)j * n;
+                } else {
+                    u64 *t = ex + ((size_t)j * (l + 1) + ii) * n;
+                    const u64 *d = dig + (size_t)j * n;
+                    const u64 qj = c->P.q[j], hj = (qj - 1) / 2;
+                    for (u32 x = 0; x < n; x++) t[x] = d[x] > hj ? smod(-(i64)(qj - d[x]), q) : d[x] % q;
+                    ntt(t, &c->M[pi], n);
+                    e = t;
+                }
+                const u64 *kb = key->data + (((size_t)j * 2 + 0) * (L + 1) + pi) * n;
+                const u64 *ka = key->data + (((size_t)j * 2 + 1) * (L + 1) + pi) * n;
+                for (u32 x = 0; x < n; x++) {
+                    a0[x] = addmod(a0[x], mulmod(e[x], kb[x], q), q);
+                    a1[x] = addmod(a1[x], mulmod(e[x], ka[x], q), q);
+                }
+            }
+        }
+        for (u32 p = 0; p < 2; p++) intt(acc + (size_t)(p * (l + 1) + l) * n, &c->M[L], n);
+    }
+    free(c1r);
+    return 0;
+}

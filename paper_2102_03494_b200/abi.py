@@ -104,6 +104,7 @@ SIGNATURES = {
     "fhe_rotate_and_sum": (c_int, [c_void_p, _VPP, _VPP, c_uint32, c_uint32]),
     "fhe_combine": (c_int, [c_void_p, _VPP, POINTER(c_uint32), c_uint32, c_void_p]),
     "fhe_ct_gemm": (c_int, [c_void_p, _VPP, c_uint32, POINTER(c_int64), c_uint32, _VPP]),
+    "fhe_debug_rotate_stages": (c_int, [c_void_p, c_void_p, c_uint32, _U64P, _U64P, _U64P]),
 }
 
 

@@ -1707,6 +1707,63 @@ static int check_rot(fhe_ctx *c, u32 k) {
     return 0;
 }
 
+// Test access to the stages of a rotation's key switch: the product pipeline (gather + INTT,
+// ModUp, inner products, special-row INTT) on one sub-batch, without the c0 addend, with the
+// workspaces copied out (ffconv_he.h: fhe_debug_rotate_stages).
+extern "C" int fhe_debug_rotate_stages(fhe_ctx *c, const fhe_ct *a, uint32_t k, uint64_t *digits, uint64_t *ext,
+                                       uint64_t *acc) {
+    TRY(check_rot(c, k));
+    if (ks_fused_ok(c)) return fail(FHE_EINVAL, "debug_rotate_stages: the fused key switch keeps no stages");
+    const int S = (int)a->count;
+    if (S > c->S) return fail(FHE_EINVAL, "debug_rotate_stages: at most %d physical ciphertexts", c->S);
+    const u32 l = a->level, g = galois_elt(c, k);
+    const size_t n = c->n, stride = 2ull * l * n;
+    use_lane(c, 0);
+    const u64 *key;
+    c->key_tick++;
+    TRY(get_key(c, g, &key));
+    fhe_ct *scratch = nullptr;
+    TRY(fhe_ct_create(c, a->R, l, &scratch));
+    PtrTab pt;
+    memset(&pt, 0, sizeof pt);
+    for (int s = 0; s < S; s++) { pt.in[s] = a->d + s * stride; pt.out[s] = scratch->d + s * stride; pt.g[s] = g; }
+    LOGN_SWITCH(c->logn, launch_row<LG, true>(c, "k_rot_gather_intt", k_rot_gather_intt<LG>, dim3(S, l), c->st,
+                                              pt, (int)l, c->w_D, c->d_mods));
+    DigitTab dt;
+    KsOut ko;
+    memset(&dt, 0, sizeof dt);
+    memset(&ko, 0, sizeof ko);
+    for (int s = 0; s < S; s++) {
+        dt.coef[s] = c->w_D + (size_t)s * l * n;
+        dt.ntt[s] = a->d + s * stride + (size_t)l * n;
+        dt.dperm[s] = g;
+        dt.key[s] = key;
+        ko.out[s] = scratch->d + s * stride;
+    }
+    ko.out_pstride = (long long)l * n;
+    ko.add_pmask = 0;
+    cudaMemsetAsync(c->w_Ext, 0, (size_t)S * l * (l + 1) * n * 8, c->st);      // the diagonal stays zero
+    int rc = keyswitch_modup(c, S, l, dt);
+    if (!rc) rc = keyswitch_tail(c, S, l, dt, ko);
+    if (!rc) {
+        cudaMemcpyAsync(digits, c->w_D, (size_t)S * l * n * 8, cudaMemcpyDeviceToHost, c->st);
+        cudaMemcpyAsync(ext, c->w_Ext, (size_t)S * l * (l + 1) * n * 8, cudaMemcpyDeviceToHost, c->st);
+        cudaMemcpyAsync(acc, c->w_Acc, (size_t)S * 2 * (l + 1) * n * 8, cudaMemcpyDeviceToHost, c->st);
+        if (cudaStreamSynchronize(c->st) != cudaSuccess) rc = fail(FHE_EDEVICE, "debug_rotate_stages: copy failed");
+    }
+    fhe_ct_destroy(scratch);
+    if (rc) return rc;
+    // ModUp leaves lazy representatives (< B q): canonical form for the comparison
+    for (int s = 0; s < S; s++)
+        for (u32 j = 0; j < l; j++)
+            for (u32 i = 0; i <= l; i++) {
+                const u64 q = i == l ? c->P.p[0] : c->P.q[i];
+                u64 *row = ext + (((size_t)s * l + j) * (l + 1) + i) * n;
+                for (size_t x = 0; x < n; x++) row[x] %= q;
+            }
+    return 0;
+}
+
 extern "C" int fhe_rotate(fhe_ctx *c, const fhe_ct *a, uint32_t k, fhe_ct *out) {
     TRY(check_rot(c, k));
     if (!same_shape(a, out)) return fail(FHE_ELEVEL, "rotate: shape/level mismatch");

@@ -236,14 +236,22 @@ DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, i
 }
 // E consecutive words of one thread to / from global memory with 32-byte accesses
 // (p 32-byte aligned for E >= 4)
+#ifndef NTT_STORE_VEC
+#define NTT_STORE_VEC 4     // words per store of store_keep: 4 (32-byte stores, measured best) or 2 (16-byte)
+#endif
 template <int E>
 DEV void store_keep(u64 *p, const u64 (&v)[E]) {
-    if constexpr (E % 4 == 0) {
+    if constexpr (E % 4 == 0 && NTT_STORE_VEC == 4) {
 #pragma unroll
         for (int e = 0; e < E; e += 4)
             asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p + e), "l"(v[e]), "l"(v[e + 1]), "l"(v[e + 2]),
                          "l"(v[e + 3])
                          : "memory");
+    } else if constexpr (E % 2 == 0) {
+        // 16-byte stores: the two outputs of one last-stage butterfly, where the register
+        // allocator can place them without staging moves
+#pragma unroll
+        for (int e = 0; e < E; e += 2) *reinterpret_cast<ulonglong2 *>(p + e) = make_ulonglong2(v[e], v[e + 1]);
     } else {
 #pragma unroll
         for (int e = 0; e < E; e++) p[e] = v[e];
@@ -254,9 +262,9 @@ DEV void load_keep(u64 (&v)[E], const u64 *p) {
     if constexpr (E % 4 == 0) {
 #pragma unroll
         for (int e = 0; e < E; e += 4)
-            asm volatile("ld.global.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
-                         : "=l"(v[e]), "=l"(v[e + 1]), "=l"(v[e + 2]), "=l"(v[e + 3])
-                         : "l"(p + e));
+            asm("ld.global.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+                : "=l"(v[e]), "=l"(v[e + 1]), "=l"(v[e + 2]), "=l"(v[e + 3])
+                : "l"(p + e));
     } else {
 #pragma unroll
         for (int e = 0; e < E; e++) v[e] = p[e];

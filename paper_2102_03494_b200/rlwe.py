@@ -330,6 +330,16 @@ class Evaluator:
                       handle_array([o.ptr for o in outs]))
         return outs
 
+    def debug_rotate_stages(self, ct: Ciphertext, k: int):
+        """(digits [c][l][n], ext [c][l][l+1][n], acc [c][2][l+1][n]) of rotate(ct, k)'s key
+        switch, c = T * rows physical ciphertexts (fhe_debug_rotate_stages; tests only)."""
+        c, l = self.T * ct.rows, ct.level
+        digits = np.empty((c, l, self.n), dtype=np.uint64)
+        ext = np.empty((c, l, l + 1, self.n), dtype=np.uint64)
+        acc = np.empty((c, 2, l + 1, self.n), dtype=np.uint64)
+        self.lib.call("fhe_debug_rotate_stages", self.ctx, ct.ptr, int(k), u64_ptr(digits), u64_ptr(ext), u64_ptr(acc))
+        return digits, ext, acc
+
     def copy(self, src: Ciphertext, dst: Ciphertext) -> None:
         """dst <- src words on the device (same rows and level), asynchronous."""
         self.lib.call("fhe_ct_copy", self.ctx, src.ptr, dst.ptr)

@@ -130,3 +130,30 @@ def test_composite_operator_errors(golden_lib):
         ev.combine([a, a], [5, 4])                 # 9 slots > N = 8
     with pytest.raises(FheError):
         ev.combine([a, a], [0, 4])                 # empty payload
+
+
+def test_debug_rotate_stages_are_the_rotation(golden_lib):
+    """The stages fhe_debug_rotate_stages exposes recombine into fhe_rotate's output:
+    ModDown(acc) + tau_g(c0) (the GPU parity test compares the stages themselves)."""
+    P = make_params(32, [65537], levels=3, q_bits=50)
+    ev = Evaluator(P, golden_lib)
+    rng = np.random.default_rng(8)
+    ct = ev.encrypt(_slots(P, 1, rng))
+    digits, ext, acc = ev.debug_rotate_stages(ct, 5)
+    l, n = ct.level, P.n
+    assert digits.shape == (1, l, n) and ext.shape == (1, l, l + 1, n) and acc.shape == (1, 2, l + 1, n)
+    for j in range(l):
+        assert not ext[0, j, j].any()                       # diagonal: read from the input
+        assert int(digits[0, j].max()) < int(P.q[j])
+    # c1 of the rotation is ModDown(acc[1]): (acc_i - [special row lifted]_i) / P mod q_i in the NTT domain,
+    # so in the coefficient domain P * c1 + lift(special) == acc; check one prime at one evaluation-free point:
+    # the sum of all NTT values of a row is n * coefficient 0
+    out = ev.read(ev.rotate(ct, 5))[0]
+    Pm = int(P.p[0])
+    for i in range(l):
+        q = int(P.q[i])
+        r0 = int(acc[0, 1, l, 0])
+        r0 = r0 - Pm if r0 > (Pm - 1) // 2 else r0
+        lhs = (sum(int(v) for v in acc[0, 1, i]) - n * r0) % q
+        rhs = (Pm * sum(int(v) for v in out[1, i])) % q
+        assert lhs == rhs

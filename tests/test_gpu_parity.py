@@ -325,3 +325,26 @@ def test_ct_gemm_wide_k_on_gpu(golden_lib, cuda_lib):
     w = rng.integers(-(1 << 40), 1 << 40, size=(K, O))
     for og, oc in zip(gd.ct_gemm(gi, w.tolist()), gp.ct_gemm(ci, w.tolist())):
         assert np.array_equal(gd.read(og), gp.read(oc))
+
+
+@pytest.mark.parametrize("case", [CASES[1], CASES[4], CASES[6], CASES[7], CASES[8], CASES[-2]],
+                         ids=lambda c: f"N{c[0]}-T{len(c[1])}-L{c[2]}-q{c[3]}")
+def test_key_switch_stages_bit_exact(case, golden_lib, cuda_lib):
+    """Parity after every KERNEL of a rotation, not only after the primitive: the digits
+    (k_rot_gather_intt), the extended digits (k_modup), the key inner products
+    (k_ks_inner) and the special row in coefficient form (k_ks_special) equal the golden
+    model's intermediates word for word."""
+    gd, gp, P = _pair(case, golden_lib, cuda_lib)
+    rng = np.random.default_rng(21)
+    s = _rand_slots(P, 2, rng)
+    cg = gd.encrypt(s, nonce=9)
+    cc = gp.new_ct(2)
+    gp.write(cc, gd.read(cg))
+    k = max(1, P.n_slots // 2 - 1)
+    for name, g, c in zip(("digits", "ext", "acc"), gd.debug_rotate_stages(cg, k), gp.debug_rotate_stages(cc, k)):
+        assert np.array_equal(g, c), name
+    # and a lower level (fewer digits than the keys were generated for)
+    if P.L > 2:
+        lg, lc = gd.mod_switch(cg), gp.mod_switch(cc)
+        for name, g, c in zip(("digits", "ext", "acc"), gd.debug_rotate_stages(lg, 1), gp.debug_rotate_stages(lc, 1)):
+            assert np.array_equal(g, c), name
