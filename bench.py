@@ -911,9 +911,12 @@ def _ncu_traffic(kernel: str):
     committed `ncu --set full` summary in profiles/ (None if absent)."""
     import glob
     import re
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_prof_top.txt")), reverse=True):
+    base = kernel.split("(")[0]
+    paths = glob.glob(os.path.join(ROOT, "profiles", f"r*_{base}.txt")) + \
+        glob.glob(os.path.join(ROOT, "profiles", "r*_prof_top.txt"))
+    for path in sorted(paths, key=os.path.basename, reverse=True):
         text = open(path).read()
-        if kernel.split("(")[0] not in text.splitlines()[0]:
+        if base not in "\n".join(text.splitlines()[:6]):
             continue
         vals = {}
         for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
