@@ -238,7 +238,7 @@ struct DigitTab {
 // Key switching, step 2 (ModUp).  grid (S, l, l+1): digit j of ct s lifted (centered)
 // into prime i (i == l: the special prime) and transformed; the diagonal i == j is
 // skipped (the inner product reads it from DigitTab.ntt).
-template <int LOGN>
+template <int LOGN, bool PERSIST = false>
 DEV void modup_row(const DigitTab &dt, u64 *Ext, int l, int special_id, const ModInfo *__restrict__ mods, int s, int j,
                    int i, u64 *sm, int tid) {
     using C = RowCfg<LOGN, false, FwdW5<LOGN>::value>;
@@ -259,18 +259,18 @@ DEV void modup_row(const DigitTab &dt, u64 *Ext, int l, int special_id, const Mo
         for (int e = 0; e < C::E; e++) v[e] = centered_lift_lazy(ld_stream(src + C::io(tid, e)), half_j, qj_mod, M);
     }
     u64 *dst = Ext + (((long long)s * l + j) * (l + 1) + i) * n + C::base();
-    if constexpr (C::CL == 0 && LOGN >= 5) {
-        // single-CTA rows: the last pass's results go from the registers straight to global
-        // memory (32 consecutive words per thread, 32-byte stores): no staging pass, and the
-        // shared memory is free for the next row without another barrier
-        const int B = ntt_fwd_core<LOGN, C::W, false, true>(v, sm, M, tid);
-        if (!((u128)(l + 2) * (u64)B * M.q < ((u128)1 << 64))) {
+    if constexpr (C::CL == 0 && C::TH >= 32 && C::Loc::NP > 1) {
+        // single-CTA rows: every warp copies out its own chunk of the last pass (coalesced
+        // 8-byte stores) behind a warp barrier only; PERSIST: rows follow each other in the CTA
+        const int B = ntt_fwd_core<LOGN, C::W, false, OUT_WARP, PERSIST>(v, sm, M, tid);
+        const int x0 = warp_chunk_base<C::W>(tid) + (tid & 31);
+        if ((u128)(l + 2) * (u64)B * M.q < ((u128)1 << 64)) {
 #pragma unroll
-            for (int e = 0; e < C::E; e++) v[e] = red_any(v[e], M.q, M.mu, M.nq);
+            for (int k = 0; k < C::E; k++) dst[x0 + 32 * k] = sm[C::pad(x0 + 32 * k)];
+        } else {
+#pragma unroll
+            for (int k = 0; k < C::E; k++) dst[x0 + 32 * k] = red_any(sm[C::pad(x0 + 32 * k)], M.q, M.mu, M.nq);
         }
-        // (stores interleaved with the last stage -- per butterfly or per four outputs -- were
-        // measured 11-15 % slower than this block of 32-byte stores after it)
-        store_keep<C::E>(dst + ((long long)tid << C::W), v);
         return;
     }
     const int B = ntt_fwd_row<LOGN, false, FwdW5<LOGN>::value>(v, sm, M, tid);
@@ -311,10 +311,10 @@ __global__ void __launch_bounds__(RowCfg<LOGN, false, FwdW5<LOGN>::value>::TH) k
             const u64 *nsrc = dt.coef[sn] + (long long)jn * C::N;
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nsrc), "r"((u32)(C::N * 8)) : "memory");
         }
-        modup_row<LOGN>(dt, Ext, l, special_id, mods, s, j, i, sm, tid);
-        // no barrier: the row's last shared-memory reads are fenced inside the NTT core (its
-        // results leave from the registers), so warps run ahead into the next row's loads
-        if constexpr (LOGN < 5) __syncthreads();
+        // no barrier here: the NTT core fences the next row's first shared-memory store
+        // (PRESYNC), so warps run ahead into the next row's loads and first pass while
+        // others still copy out
+        modup_row<LOGN, true>(dt, Ext, l, special_id, mods, s, j, i, sm, tid);
     }
 }
 
@@ -370,8 +370,9 @@ DEV void rescale_row(const RescaleArgs &a, const ModInfo *__restrict__ mods, int
                          "r"((u32)(C::N * 8))
                          : "memory");
         // single-CTA rows: the NTT's last pass stays in the registers (E consecutive words
-        // per thread) and the epilogue runs on them with 32-byte global accesses
-        const int B = ntt_fwd_core<LOGN, C::W, false, true>(v, sm, M, tid);
+        // per thread) and the epilogue runs on them with 32-byte global accesses (the
+        // warp-fenced shared-memory form ModUp uses measured 3.7 % slower here)
+        const int B = ntt_fwd_core<LOGN, C::W, false, OUT_REGS>(v, sm, M, tid);
         const long long o = (long long)tid << C::W;
         const bool lazy = (u128)(B + 1) * M.q < ((u128)1 << 64);
         const u64 Bq = (u64)B * M.q;

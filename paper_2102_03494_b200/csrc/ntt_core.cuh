@@ -79,6 +79,9 @@ struct InvLazy {
     }
 };
 
+#ifndef NTT_EXP
+#define NTT_EXP 0
+#endif
 #ifndef NTT_W_FWD
 #define NTT_W_FWD 4
 #endif
@@ -186,11 +189,18 @@ DEV int fidx(int tid, int e, int f0) {
 // with __syncthreads().
 // CANON = false: the outputs are left lazy; the return value is their bound in
 // units of q (every output < bound * q <= 2^64), for callers that absorb it.
-// KEEP = true: the last pass leaves its results in the registers instead of shared memory
-// (no final store and barrier): v[e] = out[(tid << W) | e], E consecutive words per thread,
-// for callers that store or post-process them from there (store_keep / load_keep below).
-// Shared memory is then free for the next row as soon as this call returns.
-template <int LOGN, int WW = DefaultW<LOGN>::value, bool CANON = true, bool KEEP = false>
+// OUT selects where the last pass leaves its results:
+//   OUT_SMEM  shared memory, fenced by __syncthreads() (any thread may read any word);
+//   OUT_REGS  the registers (no final store and barrier): v[e] = out[(tid << W) | e], E
+//             consecutive words per thread (store_keep / load_keep below);
+//   OUT_WARP  shared memory, fenced by __syncwarp() only: a warp's 32 E words are one
+//             contiguous chunk written by that warp alone, so each warp reads back ITS chunk
+//             (warp_chunk_base + k * 32 + lane: coalesced global accesses) without waiting
+//             for the others -- the warps' epilogues and the next row's first pass overlap.
+// PRESYNC (persistent callers of OUT_WARP): a barrier before the first shared-memory store
+// of the row, so no warp is still reading its chunk of the previous row.
+enum { OUT_SMEM = 0, OUT_REGS = 1, OUT_WARP = 2 };
+template <int LOGN, int WW = DefaultW<LOGN>::value, bool CANON = true, int OUT = OUT_SMEM, bool PRESYNC = false>
 DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, int tid) {
     using C = NttCfg<LOGN, WW>;
     constexpr int W = C::W, E = C::E, NP = C::NP;
@@ -200,10 +210,16 @@ DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, i
         const int s0 = p * W;
         const int f0 = (LOGN - s0 - W) > 0 ? (LOGN - s0 - W) : 0;
         const int k = (LOGN - s0) < W ? (LOGN - s0) : W;
+        // The exchange into the last pass is warp-local: in pass NP-2 a warp writes exactly the
+        // 32 E consecutive words it reads (and rewrites) in pass NP-1, so both of its fences
+        // are warp barriers and the warps drift apart (one's exchange under another's
+        // butterflies).  WL: the configuration has whole warps.
+        constexpr bool WL = C::TH >= 32 && NP >= 2;
         if (p > 0) {
 #pragma unroll
             for (int e = 0; e < E; e++) v[e] = sm[C::pad(fidx<W>(tid, e, f0))];
-            __syncthreads();
+            if (WL && p == NP - 1) __syncwarp();
+            else __syncthreads();
         }
 #pragma unroll
         for (int ls = 0; ls < k; ls++) {
@@ -216,24 +232,39 @@ DEV int ntt_fwd_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, i
                     if (!(e & (1 << b))) v[e] = Lz.cred(v[e]);
             }
             ulonglong2 tw[E / 2];
+#if NTT_EXP == 1      // timing experiment: no twiddle loads (results are garbage)
+#pragma unroll
+            for (int d = 0; d < E / 2; d++) tw[d] = make_ulonglong2(M.ninv + d, M.ninv_sh + s);
+#else
             fetch_tw(tw, M.tw + (1u << s) + ((u32)fidx<W>(tid, 0, f0) >> (LOGN - s)), E >> (b + 1), s);
+#endif
 #pragma unroll
             for (int e = 0; e < E; e++) {
                 if (e & (1 << b)) continue;
+#if NTT_EXP == 2      // timing experiment: no butterfly arithmetic (results are garbage)
+                v[e] ^= tw[e >> (b + 1)].x;
+                v[e | (1 << b)] += tw[e >> (b + 1)].y;
+#else
                 Lz.bfly(v[e], v[e | (1 << b)], tw[e >> (b + 1)]);
+#endif
             }
         }
         if (CANON && p == NP - 1) {
 #pragma unroll
             for (int e = 0; e < E; e++) v[e] = red_any(v[e], M.q, M.mu, M.nq);
         }
-        if (KEEP && p == NP - 1) break;
+        if (OUT == OUT_REGS && p == NP - 1) break;
+        if (PRESYNC && p == 0) __syncthreads();
 #pragma unroll
         for (int e = 0; e < E; e++) sm[C::pad(fidx<W>(tid, e, f0))] = v[e];
-        __syncthreads();
+        if ((OUT == OUT_WARP && p == NP - 1 && NP > 1) || (WL && p == NP - 2)) __syncwarp();
+        else __syncthreads();
     }
     return CANON ? 1 : Lz.B;
 }
+// first word of the chunk the thread's warp owns after an OUT_WARP transform
+template <int W>
+DEV int warp_chunk_base(int tid) { return (tid & ~31) << W; }
 // E consecutive words of one thread to / from global memory with 32-byte accesses
 // (p 32-byte aligned for E >= 4)
 #ifndef NTT_STORE_VEC
@@ -291,7 +322,14 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
 #pragma unroll
             for (int e = 0; e < E; e++) v[e] = sm[C::pad(fidx<W>(tid, e, f0))];
         }
-        if (p < NP - 1) __syncthreads();
+        // Mirror image of the forward core: passes 0 and 1 both work on the warp's own 32 E
+        // consecutive words, so the fences around that exchange are warp barriers (pass 0's
+        // only when it does not gather through an automorphism).
+        constexpr bool WL = C::TH >= 32 && NP >= 3 && 2 * W <= LOGN;
+        if (p < NP - 1) {
+            if (WL && (p == 1 || (p == 0 && !g_perm))) __syncwarp();
+            else __syncthreads();
+        }
 #pragma unroll
         for (int ls = 0; ls < k; ls++) {
             const int lt = lt0 + ls;
@@ -320,7 +358,8 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
         if (p < NP - 1) {
 #pragma unroll
             for (int e = 0; e < E; e++) sm[C::pad(fidx<W>(tid, e, f0))] = v[e];
-            __syncthreads();
+            if (WL && p == 0) __syncwarp();
+            else __syncthreads();
         }
     }
 }
