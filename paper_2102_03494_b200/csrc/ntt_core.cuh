@@ -9,9 +9,8 @@
 // butterfly stages per pass; passes exchange through shared memory padded one
 // word per 2^W (conflict-free for 64-bit accesses).  Default W = 4 (radix-16,
 // 1024 threads x 64 registers for n = 2^14, 139 KB of shared memory) for both
-// directions: standalone, W = 5 is 2-5 % faster, but inside the fused row kernels
-// (ModUp, ModDown, the rotation's gather + INTT) W = 4 wins -- the radix-32 inverse
-// kernels are ~105 KB of SASS and stall on instruction fetch (profiles/r01_*).
+// directions and every fused row kernel: radix-32 passes (W = 5, kept as a per-kernel
+// knob) measured slower once the warp-local exchange fences were in.
 // Butterfly values are kept lazily bounded (FwdLazy / InvLazy below) and reduced
 // once at the end.
 #pragma once
@@ -384,8 +383,8 @@ DEV void ntt_inv_core(u64 (&v)[NttCfg<LOGN, WW>::E], u64 *sm, const ModInfo &M, 
 #ifndef NTT_LOGL_BIG
 #define NTT_LOGL_BIG 14  // words per CTA of the cluster rows (n = 2^15, 2^16)
 #endif
-// WO != 0 overrides the radix of single-CTA rows (k_modup and k_ntt_rows run radix-32
-// forward passes: they are faster there, k_rescale is not -- DESIGN.md section 5)
+// WO != 0 overrides the radix of single-CTA rows, per kernel (FwdW5 for k_modup /
+// k_ntt_rows, RescaleW for k_rescale: all radix-16 now, see the header comment)
 template <int LOGN, bool INV, int WO = 0>
 struct RowCfg {
     static constexpr int LOGL = LOGN > 14 ? NTT_LOGL_BIG : (LOGN > NTT_LOGL ? NTT_LOGL : LOGN);    // log2 words per CTA
@@ -571,7 +570,7 @@ DEV int ntt_fwd_row(u64 (&v)[RowCfg<LOGN, false, WO>::E], u64 *sm, const ModInfo
     else return ntt_fwd_cluster<LOGN, CANON, WO>(v, sm, M, tid);
 }
 #ifndef NTT_W_FUSED_FWD
-#define NTT_W_FUSED_FWD 5
+#define NTT_W_FUSED_FWD 4
 #endif
 template <int LOGN>
 struct FwdW5 {       // radix override for k_modup / k_ntt_rows
