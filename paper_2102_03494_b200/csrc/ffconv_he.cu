@@ -1449,8 +1449,15 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     const bool fold = (u128)(l + 2) * maxq < ((u128)1 << 64);
     KsAdd kad;
     memset(&kad, 0, sizeof kad);
+    // Both addends fold into the inner product.  FHE_FOLD_ACC=0 leaves the rotate-and-add
+    // addend (the input ciphertext, no automorphism) to the ModDown epilogue instead: measured
+    // equal in kernel time (k_ks_inner -177 ms, k_rescale +178 ms per configs[2] chunk) and
+    // 2.6 % slower overall.
+    static int fold_acc = -1, fused_env = -1;
+    if (fused_env < 0) { const char *e = getenv("FHE_FUSED_MODDOWN"); fused_env = e ? atoi(e) : 0; }
+    if (fold_acc < 0) { const char *e = getenv("FHE_FOLD_ACC"); fold_acc = (e ? atoi(e) : 1) || fused_env; }   // k_moddown folds both
     if (fold) {
-        for (int s = 0; s < S; s++) { kad.add[s] = ko.add[s]; kad.add_g[s] = ko.add_g[s]; kad.acc[s] = ko.acc[s]; }
+        for (int s = 0; s < S; s++) { kad.add[s] = ko.add[s]; kad.add_g[s] = ko.add_g[s]; kad.acc[s] = fold_acc ? ko.acc[s] : nullptr; }
         kad.add_pstride = ko.add_pstride;
         kad.acc_pstride = ko.acc_pstride;
         kad.add_pmask = ko.add_pmask;
@@ -1459,8 +1466,6 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     // FHE_FUSED_MODDOWN=1: the q primes' inner product runs in k_moddown's epilogue instead
     // of a separate k_ks_inner pass (needs the addend fold).  Off by default: measured 3 %
     // slower (the epilogue serialises behind the NTT in each CTA)
-    static int fused_env = -1;
-    if (fused_env < 0) { const char *e = getenv("FHE_FUSED_MODDOWN"); fused_env = e ? atoi(e) : 0; }
     const bool fused = fold && fused_env != 0;
     if (!fused) {
         ProfScope ps_(c, "k_ks_inner");
@@ -1493,7 +1498,8 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
         ra.coef[s] = c->w_Acc + ((size_t)s * 2 * (l + 1) + l) * n;
         ra.base[s] = c->w_Acc + (size_t)s * 2 * (l + 1) * n;
         ra.out[s] = ko.out[s];
-        if (!fold) { ra.add[s] = ko.add[s]; ra.add_g[s] = ko.add_g[s]; ra.acc[s] = ko.acc[s]; }
+        if (!fold) { ra.add[s] = ko.add[s]; ra.add_g[s] = ko.add_g[s]; }
+        if (!fold || !fold_acc) ra.acc[s] = ko.acc[s];
     }
     ra.coef_pstride = (long long)(l + 1) * n;
     ra.base_pstride = (long long)(l + 1) * n;
@@ -1501,8 +1507,8 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
     if (!fold) {
         ra.add_pstride = ko.add_pstride;
         ra.add_pmask = ko.add_pmask;
-        ra.acc_pstride = ko.acc_pstride;
     }
+    ra.acc_pstride = ko.acc_pstride;
     ra.src_id = c->special_id;
     for (u32 i = 0; i < l; i++) { ra.fac[i] = c->pinv[i]; ra.fac_sh[i] = c->pinv_sh[i]; }
     if (fused) {
