@@ -451,9 +451,12 @@ DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false, WO>::E], u64 *sm, const Mod
         const int s0 = S0 + p * W;
         const int f0 = (LOGL - s0 - W) > 0 ? (LOGL - s0 - W) : 0;
         const int k = (LOGL - s0) < W ? (LOGL - s0) : W;
+        // warp-local exchange into the last local pass, as in the single-CTA core
+        constexpr bool WL = R::TH >= 32 && NP >= 2;
 #pragma unroll
         for (int e = 0; e < E; e++) v[e] = sm[R::pad(fidx<W>(tid, e, f0))];
-        __syncthreads();
+        if (WL && p == NP - 1) __syncwarp();
+        else __syncthreads();
 #pragma unroll
         for (int ls = 0; ls < k; ls++) {
             const int sl = s0 + ls;
@@ -479,7 +482,8 @@ DEV int ntt_fwd_cluster(u64 (&v)[RowCfg<LOGN, false, WO>::E], u64 *sm, const Mod
         }
 #pragma unroll
         for (int e = 0; e < E; e++) sm[R::pad(fidx<W>(tid, e, f0))] = v[e];
-        __syncthreads();
+        if (WL && p == NP - 2) __syncwarp();
+        else __syncthreads();
     }
     return CANON ? 1 : Lz.B;
 }
@@ -501,9 +505,12 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
         const int lt0 = p * W;
         const int k = (LT - lt0) < W ? (LT - lt0) : W;
         const int f0 = lt0 < LOGL - W ? lt0 : LOGL - W;
+        // warp-local exchange between the first two local passes, as in the single-CTA core
+        constexpr bool WL = R::TH >= 32 && NP >= 3 && 2 * W <= LOGL;
 #pragma unroll
         for (int e = 0; e < E; e++) v[e] = sm[R::pad(fidx<W>(tid, e, f0))];
-        __syncthreads();
+        if (WL && p <= 1) __syncwarp();
+        else __syncthreads();
 #pragma unroll
         for (int ls = 0; ls < k; ls++) {
             const int lt = lt0 + ls;
@@ -525,7 +532,8 @@ DEV void ntt_inv_cluster(u64 (&v)[RowCfg<LOGN, true>::E], u64 *sm, const ModInfo
         }
 #pragma unroll
         for (int e = 0; e < E; e++) sm[R::pad(fidx<W>(tid, e, f0))] = v[e];
-        __syncthreads();
+        if (WL && p == 0) __syncwarp();
+        else __syncthreads();
     }
     cl.sync();   // all local stages of the row are done
 #pragma unroll
