@@ -604,7 +604,9 @@ static int setup_workspace(fhe_ctx *c) {
     // sub-batch: as many ciphertexts as 1.25 GB of workspace per lane holds, at most MAXS
     // (128 measured best at configs[1]: fewer partial waves of the row kernels;
     // profiles/r02_subbatch.json)
-    size_t budget = 1280ull << 20;
+    // (rings 2^15 / 2^16 keep the 512 MB budget: their ciphertext objects are GBs and
+    // the engine's output groups are sized against what the workspaces leave)
+    size_t budget = (c->logn > 14 ? 512ull : 1280ull) << 20;
     const char *env = getenv("FHE_KS_BATCH");
     int S = env ? atoi(env) : (int)(budget / per_ct);
     if (!env && S < 8) S = 8;          // large rings: keep >= 8 ciphertexts per sub-batch

@@ -159,17 +159,6 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_intt_rows(InttRowsAr
             const int gi = base + i;
             sm[C::pad(i)] = addm(src[gi], mont(c1[gi], sk[gi], M.q, M.qinv), M.q);
         }
-    } else if (a.gather == 2 && C::CL == 0) {
-        // single-CTA row: stage, then permute inside shared memory
-        #pragma unroll
-        for (int i = tid, e_ = 0; e_ < C::E; i += C::TH, e_++) sm[C::pad(i)] = src[i];
-        __syncthreads();
-        u64 w[C::E];
-#pragma unroll
-        for (int e = 0; e < C::E; e++) w[e] = sm[C::pad(galois_perm(tid + e * C::TH, a.g, LOGN))];
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < C::E; e++) sm[C::pad(tid + e * C::TH)] = w[e];
     } else {
         #pragma unroll
         for (int i = tid, e_ = 0; e_ < C::E; i += C::TH, e_++) {
@@ -209,10 +198,15 @@ __global__ void __launch_bounds__(RowCfg<LOGN, true>::TH) k_rot_gather_intt(PtrT
     const ModInfo M = mods[i];
     u64 v[C::E];
     if constexpr (C::CL == 0) {
+        // The automorphism is applied on the way into shared memory: galois_perm maps every
+        // aligned block of 32 words onto an aligned block of 32 words (the high bits of
+        // perm(j) depend on the high bits of j only), so a warp's gathered loads touch the
+        // same eight sectors a straight load would, the first NTT pass reads shared memory
+        // conflict-free, and its fences stay warp-local (no gather inside the core).
         #pragma unroll
-        for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) sm[C::pad(x)] = ld_stream(src + x);
+        for (int x = tid, e_ = 0; e_ < C::E; x += C::TH, e_++) sm[C::pad(x)] = ld_stream(src + galois_perm(x, g, LOGN));
         __syncthreads();
-        ntt_inv_core<LOGN>(v, sm, M, tid, g);
+        ntt_inv_core<LOGN>(v, sm, M, tid);
     } else {
         // cluster row: the automorphism gathers across CTAs, so read it from global memory
         #pragma unroll
