@@ -950,8 +950,23 @@ extern "C" int fhe_ct_create(fhe_ctx *c, uint32_t R, uint32_t level, fhe_ct **ou
     }
     cudaError_t e = cudaMallocAsync((void **)&ct->d, words * 8, c->st);
     if (e != cudaSuccess) {
+        // The stream-ordered pool keeps freed blocks (release threshold: never) and fragments
+        // when ciphertext sizes mix (level schedule, GB-sized objects at ring 2^16): wait for
+        // the pending frees, hand the unused reservations back and try once more.
+        cudaGetLastError();
+        cudaDeviceSynchronize();
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, c->dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        e = cudaMallocAsync((void **)&ct->d, words * 8, c->st);
+    }
+    if (e != cudaSuccess) {
+        size_t fr = 0, tot = 0;
+        cudaGetLastError();
+        cudaMemGetInfo(&fr, &tot);
         delete ct;
-        return fail(FHE_ENOMEM, "ciphertext allocation of %zu bytes failed: %s", words * 8, cudaGetErrorString(e));
+        return fail(FHE_ENOMEM, "ciphertext allocation of %zu bytes failed: %s (device: %zu MB free of %zu MB; live ciphertexts %zu MB, keys %llu MB)",
+                    words * 8, cudaGetErrorString(e), fr >> 20, tot >> 20, c->live_bytes >> 20,
+                    (unsigned long long)(c->key_bytes >> 20));
     }
     c->live_bytes += words * 8;
     c->peak_bytes = std::max(c->peak_bytes, c->live_bytes);
