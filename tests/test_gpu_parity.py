@@ -348,3 +348,42 @@ def test_key_switch_stages_bit_exact(case, golden_lib, cuda_lib):
         lg, lc = gd.mod_switch(cg), gp.mod_switch(cc)
         for name, g, c in zip(("digits", "ext", "acc"), gd.debug_rotate_stages(lg, 1), gp.debug_rotate_stages(lc, 1)):
             assert np.array_equal(g, c), name
+
+
+def test_cfg1_full_batch_properties(golden_lib, cuda_lib):
+    """configs[1] at its full size: ring 2^14, 4 x 40-bit q + a 42-bit special prime, 1024 physical
+    ciphertexts in one call (8 key-switch sub-batches of 128 on two lanes).  The golden model is too
+    slow for all of them, so the whole batch is checked through size-independent properties of the
+    reference rotation (hesim.py:244-261: a cyclic shift of each slot row) and a sample of
+    ciphertexts from every sub-batch word for word against the golden model."""
+    P = make_params(8192, [1099511922689], levels=4, q_bits=40, p_bits=42)
+    gd, gp = Evaluator(P, golden_lib), Evaluator(P, cuda_lib)
+    B, N, t, k = 1024, P.n_slots, P.t[0], 5203
+    rng = np.random.default_rng(21)
+    A = rng.integers(0, t, size=(1, B, P.n), dtype=np.uint64)
+    Bm = rng.integers(0, t, size=(1, B, P.n), dtype=np.uint64)
+
+    def roll(X, s):
+        return np.concatenate([np.roll(X[..., :N], -s, axis=-1), np.roll(X[..., N:], -s, axis=-1)], axis=-1)
+
+    ca, cb = gp.encrypt(A), gp.encrypt(Bm)
+    ra, rb = gp.rotate(ca, k), gp.rotate(cb, k)
+    # the reference's slot semantics on every ciphertext of the batch
+    assert np.array_equal(gp.decrypt(ra), roll(A, k))
+    # round trip: rotating on by N - k restores every slot vector
+    assert np.array_equal(gp.decrypt(gp.rotate(ra, N - k)), A)
+    # linearity: rot(a) + rot(b) and rot(a + b) hold the same slots
+    want = roll((A + Bm) % np.uint64(t), k)
+    assert np.array_equal(gp.decrypt(gp.add(ra, rb)), want)
+    assert np.array_equal(gp.decrypt(gp.rotate(gp.add(ca, cb), k)), want)
+    # one call over many objects equals the single-object call (sub-batching is invisible)
+    parts = [gp.encrypt(A[:, r0:r0 + 256], nonce=1000 + r0) for r0 in range(0, B, 256)]
+    many = gp.rotate_many(parts, k)
+    for r0, m in zip(range(0, B, 256), many):
+        assert np.array_equal(gp.decrypt(m), roll(A[:, r0:r0 + 256], k))
+    # word-for-word against the golden model: first / last ciphertext of sub-batches on both lanes
+    rows = [0, 127, 128, 383, 640, 1023]
+    win, wout = gp.read(ca), gp.read(ra)
+    cg = gd.new_ct(len(rows))
+    gd.write(cg, win[rows])
+    assert np.array_equal(gd.read(gd.rotate(cg, k)), wout[rows])
