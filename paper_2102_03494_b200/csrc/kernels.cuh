@@ -11,7 +11,9 @@
 #define MAXQ 24
 #define MAXB 26
 #define MAXT 8
+#ifndef MAXS
 #define MAXS 128  // physical ciphertexts per key-switching sub-batch (kernel parameter tables)
+#endif
 
 struct LevelDev {
     // decryption / encryption (per plaintext modulus k)
