@@ -420,6 +420,16 @@ def run_rotation(args, rank, world, local_rank):
             "traffic_source": (_ncu_traffic(dominant) or {}).get("source"),
             "algorithmic": "per ciphertext: l*l NTTs of (n/2)log2(n) modmuls (k_modup); see DESIGN.md section 3",
         }
+    # the HBM-bound primitive of configs[1]: the fused HMA streams ct, acc in and acc out (3 x 2 l n words per
+    # ciphertext; the one plaintext of the batch, l n words, stays in L2)
+    hma_bytes = 3 * 2 * P.L * n * 8
+    hma_gbs = B * args.steps / (hma_ms * 1e-3) * hma_bytes / 1e9
+    result["roofline_hma"] = {
+        "kernel": "k_mul_plain (acc += ct * pt, in place)", "bound": "hbm", "achieved": hma_gbs,
+        "peak": _hbm_peak(), "unit": "GB/s", "frac": hma_gbs / _hbm_peak(),
+        "peak_source": "MEASURED_PEAKS.json hbm_gbs (driver-written copy bandwidth), else the recipe's fallback",
+        "traffic": None,
+        "algorithmic": f"per ciphertext: ct read + acc read + acc write = {hma_bytes} B (plaintext L2-resident)"}
     return result
 
 
