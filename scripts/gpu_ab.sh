@@ -1,9 +1,11 @@
 #!/bin/bash
-# A/B: the in-tree library against build/var/libffconv_he_head.so (parity first, then the rotation bench of both)
+# A/B: library variants (VARIANTS="build/var/libffconv_he_x.so ...") against the in-tree build:
+# the key-switch parity tests, then the configs[1] rotation bench of each.
 mkdir -p gpurun_out
-python -m pytest tests/test_gpu_parity.py -m gpu -x -q > gpurun_out/ab_parity.log 2>&1; echo "parity rc=$?"; tail -2 gpurun_out/ab_parity.log
-for tag in new head new head; do
-  lib=""; [ $tag = head ] && lib=$PWD/build/var/libffconv_he_head.so
+for lib in "" ${VARIANTS}; do
+  tag=${lib:-default}; tag=$(basename "$tag" .so); tag=${tag#libffconv_he_}
+  [ -n "$lib" ] && lib=$PWD/$lib
+  FFCONV_HE_LIB=$lib python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "key_switch_stages or cfg1_full or rotate_many or rotate_hoisted" > gpurun_out/ab_$tag.pytest 2>&1; rc=$?
   FFCONV_HE_LIB=$lib python bench.py --steps 10 --warmup 3 --no-inference > gpurun_out/ab_$tag.json 2>gpurun_out/ab_$tag.err
-  python -c "import json; d=json.load(open('gpurun_out/ab_$tag.json')); print('$tag', round(d['value']), round(d['e2e']['value']), {k: round(v['ms'],2) for k,v in d['kernels'].items()}, round(d['roofline']['frac'],4), round(d['roofline']['peak'],1))"
+  python -c "import json; d=json.load(open('gpurun_out/ab_$tag.json')); print('$tag', 'parity rc=$rc', round(d['value']), round(d['e2e']['value']), {k: round(v['ms'],2) for k,v in d['kernels'].items()}, round(d['roofline']['frac'],4))"
 done
