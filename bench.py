@@ -951,7 +951,7 @@ def _ncu_traffic(kernel: str):
     import glob
     import re
     base = kernel.split("(")[0]
-    paths = glob.glob(os.path.join(ROOT, "profiles", f"r*_{base}.txt")) + \
+    paths = glob.glob(os.path.join(ROOT, "profiles", f"r[0-9][0-9]_{base}.txt")) + \
         glob.glob(os.path.join(ROOT, "profiles", "r*_prof_top.txt"))
     for path in sorted(paths, key=os.path.basename, reverse=True):
         text = open(path).read()
