@@ -1452,10 +1452,18 @@ static int keyswitch_modup(fhe_ctx *c, int S, u32 l, const DigitTab &dt) {
 static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const KsOut &ko) {
     size_t n = c->n;
     int L = (int)c->L;
-    // inner-product variant: (ciphertexts per thread, min CTAs per SM); env FHE_KS_VARIANT=0..3
+    // inner-product variant, env FHE_KS_VARIANT (profiles/r02_subbatch.json):
+    //   0..3  register keys: (4 cts/thread, 1 CTA/SM min), (2, 1), (4, 4) [the round-2 default until the
+    //         last session], (2, 4)
+    //   6     key words in the thread's own shared-memory column, 8 cts/thread, 5 CTAs/SM
+    //   7, 9  shared-memory keys + the next ciphertext's digits prefetched (two operand sets in flight),
+    //         4 CTAs/SM, 8 / 16 cts/thread.  9 is the default: k_ks_inner -6 % at configs[1] (164.1K vs
+    //         162.1K rot/s), -11 % at configs[2] (7.44 vs 7.12 images/s on the same box)
+    // Levels above 12 (more than 48 KB of static shared memory) use variant 2.
     static int ksv = -1;
-    if (ksv < 0) { const char *e = getenv("FHE_KS_VARIANT"); ksv = e ? atoi(e) : 2; }   // 2: measured best (4 cts/thread, 4 CTAs/SM)
-    const int G = (ksv == 1 || ksv == 3) ? 2 : 4;
+    if (ksv < 0) { const char *e = getenv("FHE_KS_VARIANT"); ksv = e ? atoi(e) : 9; }
+    const bool ksm = (ksv == 6 || ksv == 7 || ksv == 9) && l <= 12;
+    const int G = ksm ? (ksv == 9 ? 16 : 8) : (ksv == 1 || ksv == 3) ? 2 : 4;
     c->alg_mm += (double)S * (2.0 * l * (l + 1) + 2.0 * l) * n;   // key inner product + ModDown scaling
     long long tot = (long long)((S + G - 1) / G) * l * n;
     // fold the addends into the inner product while its Montgomery input bound holds
@@ -1489,11 +1497,16 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
         const unsigned nb = (unsigned)nblocks(tot);
 #define KS_LAUNCH(LLV, GV, MB) k_ks_inner<LLV, GV, MB><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, \
                                                         (int)c->logn, c->special_id, c->d_mods, kad)
+#define KS_LAUNCH_SM(LLV, GV, MB, PFV) k_ks_inner<(LLV <= 12 ? LLV : 1), GV, MB, true, PFV><<<nb, 256, 0, c->st>>>(c->w_Ext, dt, c->w_Acc, S, L, \
+                                                        (int)c->logn, c->special_id, c->d_mods, kad)
 #define KS_CASE(LLV) case LLV:                                        \
-        if (ksv == 1) KS_LAUNCH(LLV, 2, 1);                           \
-        else if (ksv == 2) KS_LAUNCH(LLV, 4, 4);                      \
+        if (ksm && ksv == 7) KS_LAUNCH_SM(LLV, 8, 4, true);           \
+        else if (ksm && ksv == 9) KS_LAUNCH_SM(LLV, 16, 4, true);     \
+        else if (ksm) KS_LAUNCH_SM(LLV, 8, 5, false);                 \
+        else if (ksv == 1) KS_LAUNCH(LLV, 2, 1);                      \
         else if (ksv == 3) KS_LAUNCH(LLV, 2, 4);                      \
-        else KS_LAUNCH(LLV, 4, 1);                                    \
+        else if (ksv == 0) KS_LAUNCH(LLV, 4, 1);                      \
+        else KS_LAUNCH(LLV, 4, 4);                                    \
         break;
         switch (l) {
             KS_CASE(1) KS_CASE(2) KS_CASE(3) KS_CASE(4) KS_CASE(5) KS_CASE(6) KS_CASE(7) KS_CASE(8)
@@ -1503,6 +1516,7 @@ static int keyswitch_tail(fhe_ctx *c, int S, u32 l, const DigitTab &dt, const Ks
         }
 #undef KS_CASE
 #undef KS_LAUNCH
+#undef KS_LAUNCH_SM
     }
     CHECK_LAUNCH();
     // the special prime's inner product + ModDown INTT of both accumulators (one row each)

@@ -492,11 +492,34 @@ struct KsAdd {
     u64 pr[MAXQ];                 // P * 2^64 mod q_i (Montgomery form of P)
 };
 
-template <int LL, int KS_GROUP, int MINB>
+// KSM: the thread's 2 l key words live in its own column of shared memory instead of
+// registers (no barrier: each thread reads back only what it wrote), which frees 4 l
+// registers for a higher occupancy of this latency-bound kernel.
+template <int LL, bool KSM>
+struct KsKeys {
+    u64 kb[LL], ka[LL];
+    DEV void set(int j, u64 b, u64 a) { kb[j] = b; ka[j] = a; }
+    DEV u64 b(int j) const { return kb[j]; }
+    DEV u64 a(int j) const { return ka[j]; }
+};
+template <int LL>
+struct KsKeys<LL, true> {
+    u64 *col;            // &smem[0][threadIdx.x], row stride 256 words
+    DEV void set(int j, u64 b, u64 a) { col[j * 256] = b; col[(LL + j) * 256] = a; }
+    DEV u64 b(int j) const { return col[j * 256]; }
+    DEV u64 a(int j) const { return col[(LL + j) * 256]; }
+};
+
+// PF: the next ciphertext's extended digits are loaded before the current one's products
+// (two operand sets in flight per thread; affordable next to KSM's freed registers).
+template <int LL, int KS_GROUP, int MINB, bool KSM = false, bool PF = false>
 __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ Ext, DigitTab dt, u64 *__restrict__ Acc,
                                                      int S, int L, int logn, int special_id,
                                                      const ModInfo *__restrict__ mods, const KsAdd ka_) {
     constexpr int l = LL;
+    __shared__ u64 ksm[KSM ? 2 * LL * 256 : 1];
+    KsKeys<LL, KSM> kk;
+    if constexpr (KSM) kk.col = ksm + threadIdx.x;
     // 32-bit index math: workspace offsets stay below 2^32 words (a few GB at most)
     const u32 n = 1u << logn;
     const u32 groups = (S + KS_GROUP - 1) / KS_GROUP;
@@ -513,38 +536,42 @@ __global__ void __launch_bounds__(256, MINB) k_ks_inner(const u64 *__restrict__ 
         const ModInfo &M = mods[i];
         const u64 q = M.q, qi = M.qinv;
         const u32 kb0 = (u32)kp * n + x, ka0 = (u32)(L + 1 + kp) * n + x;
-        u64 kb[l], ka[l];
         const int sc = S - s0 < KS_GROUP ? S - s0 : KS_GROUP;
         const u64 *cur = dt.key[s0];
 #pragma unroll
-        for (int j = 0; j < l; j++) {
-            kb[j] = __ldg(cur + j * kstride + kb0);
-            ka[j] = __ldg(cur + j * kstride + ka0);
-        }
+        for (int j = 0; j < l; j++) kk.set(j, __ldg(cur + j * kstride + kb0), __ldg(cur + j * kstride + ka0));
+        u64 en[PF ? l : 1];
         for (int u = 0; u < sc; u++) {
             const int s = s0 + u;
             if (dt.key[s] != cur) {                   // a key boundary inside the group (multi-step batches)
                 cur = dt.key[s];
 #pragma unroll
-                for (int j = 0; j < l; j++) {
-                    kb[j] = __ldg(cur + j * kstride + kb0);
-                    ka[j] = __ldg(cur + j * kstride + ka0);
-                }
+                for (int j = 0; j < l; j++) kk.set(j, __ldg(cur + j * kstride + kb0), __ldg(cur + j * kstride + ka0));
             }
             // hoisted rotations share one ModUp: Ext(tau_g(c1)) = Ext(c1) read at perm_g(x)
-            const u32 xs = dt.perm[s] ? galois_perm(x, dt.perm[s], logn) : x;
-            const u32 xd = dt.dperm[s] ? galois_perm(x, dt.dperm[s], logn) : x;
-            const u32 es = dt.perm[s] ? dt.esrc[s] : (u32)s;
-            const u64 *eb = Ext + (es * l * (l + 1) + i) * n + xs;
-            const u64 *db = dt.ntt[s] + xd;
-            u64 e[l];
+            auto load_e = [&](int sx, u64(&dst)[l]) {
+                const u32 xs = dt.perm[sx] ? galois_perm(x, dt.perm[sx], logn) : x;
+                const u32 xd = dt.dperm[sx] ? galois_perm(x, dt.dperm[sx], logn) : x;
+                const u32 es = dt.perm[sx] ? dt.esrc[sx] : (u32)sx;
+                const u64 *eb = Ext + (es * l * (l + 1) + i) * n + xs;
+                const u64 *db = dt.ntt[sx] + xd;
 #pragma unroll
-            for (int j = 0; j < l; j++) e[j] = i == j ? db[j * n] : eb[j * estride];
+                for (int j = 0; j < l; j++) dst[j] = i == j ? db[j * n] : eb[j * estride];
+            };
+            u64 e[l];
+            if constexpr (PF) {
+                if (u == 0) load_e(s, en);
+#pragma unroll
+                for (int j = 0; j < l; j++) e[j] = en[j];
+                if (u + 1 < sc) load_e(s + 1, en);
+            } else {
+                load_e(s, e);
+            }
             u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
 #pragma unroll
             for (int j = 0; j < l; j++) {
-                mac128(h0, l0, e[j], kb[j]);
-                mac128(h1, l1, e[j], ka[j]);
+                mac128(h0, l0, e[j], kk.b(j));
+                mac128(h1, l1, e[j], kk.a(j));
             }
             {
                 const u64 pr = ka_.pr[i];

@@ -3,7 +3,7 @@ test_gpu_parity.py re-run in a subprocess under each environment switch the
 library reads once per process (FHE_LANES: key-switch lanes; FHE_KS_FUSED=1: ModUp
 fused into the key inner product with TMEM accumulators; FHE_FUSED_MODDOWN:
 the q primes' inner product inside the ModDown rescale; FHE_KS_BATCH: sub-batch
-size; FHE_KS_VARIANT: inner-product thread mapping)."""
+size; FHE_KS_VARIANT: inner-product thread mapping and key placement)."""
 
 import os
 import subprocess
@@ -25,6 +25,11 @@ VARIANTS = [
     {"FHE_KS_FUSED": "1"},
     {"FHE_FUSED_MODDOWN": "1", "FHE_KS_BATCH": "2"},
     {"FHE_KS_BATCH": "3", "FHE_KS_VARIANT": "1"},
+    # inner product: register keys (the earlier default), shared-memory keys without / with the
+    # prefetch of the next ciphertext's digits at 8 ciphertexts per thread (default: 9 = 16 per thread)
+    {"FHE_KS_BATCH": "11", "FHE_KS_VARIANT": "2"},
+    {"FHE_KS_BATCH": "11", "FHE_KS_VARIANT": "6"},
+    {"FHE_KS_BATCH": "19", "FHE_KS_VARIANT": "7"},
 ]
 
 
